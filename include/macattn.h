@@ -1,0 +1,154 @@
+/*
+ * macattn.h — C-ABI of the B200-native MAC-Attention decode path.
+ *
+ * The reference (`attnreuse`, /root/reference/pkg/src/attnreuse) is an
+ * in-process Python API with no FFI; the entry points below are what a
+ * binding of its hot path would call.  Each replaces one piece of
+ * `DecodeEngine.decode_step` (engine.py:410-539):
+ *
+ *   mac_append_kv     engine.py:434-437   rotate k at position m, append K/V
+ *                     (+ attention.py:212-232 rope_rotate, kvstore.py:105-119 append)
+ *                     and rotate the step's queries (engine.py:460)
+ *   mac_match         matching.py:141-175 match_query over the pre-RoPE ring,
+ *                     engine.py:449-459   with the roi / refresh gates
+ *   mac_amend         engine.py:464-470,484-493  split-KV partial summaries over
+ *                     [lo, m] cut at m-r (attention.py:75-116 summarize)
+ *   mac_complete      engine.py:471-479,486-502  cached(p) (+) piece (+) band merge
+ *                     (attention.py:119-135), output, band mass, and the ring
+ *                     write-back rectify_append (engine.py:374-402)
+ *   mac_decode_step   the four above, in stream order (one decode_step call)
+ *   mac_full_decode   append + exact attention over [1, m] (attention.py:182-189
+ *                     attend_full): the full-attention decode baseline
+ *   mac_attend_full   exact attention of R_m q over the stored [1, m], m = seq_lens
+ *                     (no append): the per-step fidelity oracle (engine.py:507-509)
+ *   mac_merge_partials  log-domain merge of per-shard (acc, lse) partials
+ *                     (attention.py:119-135 merge) for the KV-sharded miss path
+ *
+ * Conventions: plain device pointers and sizes, no allocation inside, every
+ * launch is stream-ordered and graph-capturable (no host synchronisation).
+ * Return value 0 on success, a MAC_ERR_* code for a rejected parameter set,
+ * or a cudaError_t value (< 1000) from the launch.
+ */
+#ifndef MACATTN_H_
+#define MACATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MACATTN_ABI_VERSION 1
+
+/* storage modes: dtype of the K/V cache and the query ring; summaries are
+ * f32 in MAC_MODE_F32/BF16 and f64 in MAC_MODE_F64 (engine.py:152-153 allows
+ * f32|f64; bf16 is the B200 serving storage) */
+enum { MAC_MODE_F32 = 0, MAC_MODE_BF16 = 1, MAC_MODE_F64 = 2 };
+/* element dtypes of the per-step inputs q_pre / k_pre / v */
+enum { MAC_DT_F32 = 0, MAC_DT_BF16 = 1, MAC_DT_F64 = 2 };
+/* matching.py:25-26 */
+enum { MAC_MATCH_PRE_ROPE = 0, MAC_MATCH_POST_ROPE = 1 };
+/* engine.py:41-42 */
+enum { MAC_DOWNDATE_SPLIT = 0, MAC_DOWNDATE_REMOVE = 1 };
+
+enum {
+  MAC_OK = 0,
+  MAC_ERR_NULL = 1001,      /* a required pointer is NULL */
+  MAC_ERR_SHAPE = 1002,     /* head counts / dims / window / band out of range */
+  MAC_ERR_DTYPE = 1003,     /* unknown storage mode or input dtype */
+  MAC_ERR_WORKSPACE = 1004, /* workspace smaller than mac_workspace_bytes() */
+  MAC_ERR_PAGING = 1005     /* page geometry invalid */
+};
+
+typedef struct MacDecodeParams {
+  /* ---- geometry -------------------------------------------------------- */
+  int32_t batch;         /* B requests */
+  int32_t n_q_heads;     /* Hq */
+  int32_t n_kv_heads;    /* Hkv, Hq % Hkv == 0 (engine.py:138-139) */
+  int32_t head_dim;      /* d, even (engine.py:132-133) */
+  int32_t head_dim_v;    /* d_v */
+  int32_t window;        /* W, ring capacity (engine.py:115) */
+  int32_t band;          /* r (engine.py:116) */
+  int32_t page_size;     /* tokens per KV page (kvstore.py:76) */
+  int32_t pages_per_seq; /* row stride of page_table */
+  int32_t storage;       /* MAC_MODE_* */
+  int32_t in_dtype;      /* MAC_DT_* of q_pre / k_pre / v_in */
+  int32_t max_chunks;    /* split-KV partial slots per (request, kv head) */
+  int32_t min_chunk;     /* minimum tokens per split */
+  int32_t kv_offset;     /* tokens of this request held by earlier KV shards (0 unless sharded) */
+  /* ---- match rule (matching.py:58-64, 141-175; engine.py:452-459) ----- */
+  double thr_sq;         /* (sqrt(2d)(1 - tau_layer))^2 */
+  int32_t delta_max;     /* <= 0: off */
+  int32_t match_space;   /* MAC_MATCH_* */
+  int32_t refresh_every; /* 0: off */
+  int32_t roi_gate;      /* break_even_gate (engine.py:57-63) */
+  double roi_b_kv;
+  double roi_b_q;
+  int32_t downdate;      /* MAC_DOWNDATE_* */
+  int32_t force_miss;    /* 1: every head takes the miss path */
+  double eps_cancel;     /* remove() guard (attention.py:142) */
+  /* ---- persistent state (device) --------------------------------------- */
+  int32_t* seq_lens;          /* [B] tokens stored before this step; the step stores m = seq_lens+1 */
+  const int32_t* page_table;  /* [B, pages_per_seq] physical page ids */
+  void* k_cache;              /* [num_pages, Hkv, page_size, d]   post-RoPE keys, storage dtype */
+  void* v_cache;              /* [num_pages, Hkv, page_size, d_v] values, storage dtype */
+  void* ring_q;               /* [B, Hq, W, d]   pre-RoPE queries, storage dtype */
+  void* ring_acc;             /* [B, Hq, W, d_v] prefix summary acc (f32 | f64) */
+  void* ring_lse;             /* [B, Hq, W]      prefix summary lse (-inf: empty) */
+  const double* rope_freqs;   /* [d/2] omega_j = base^(-2j/d) (attention.py:208-209) */
+  /* ---- per-step inputs (device) ---------------------------------------- */
+  const void* q_pre;          /* [B, Hq, d]   pre-RoPE queries */
+  const void* k_pre;          /* [B, Hkv, d]  pre-RoPE keys */
+  const void* v_in;           /* [B, Hkv, d_v] values */
+  /* ---- per-step outputs (device) --------------------------------------- */
+  void* out;                  /* [B, Hq, d_v] attention output (f32 | f64) */
+  int32_t* match_hit;         /* [B, Hq] raw match decision (MatchResult.hit) */
+  int32_t* use_hit;           /* [B, Hq] decision after the gates (reuse taken) */
+  int32_t* match_pos;         /* [B, Hq] p, -1 on a raw miss */
+  double* match_dist;         /* [B, Hq] best squared distance, +inf if nothing scanned */
+  int32_t* match_scanned;     /* [B, Hq] candidates scanned */
+  void* full_lse;             /* [B, Hq] lse of the full summary (f32 | f64) */
+  void* band_mass;            /* [B, Hq] rho = exp(band.lse - full.lse) (f32 | f64) */
+  void* cached_acc;           /* optional [B, Hq, d_v]: summary reused at p (NULL: not written) */
+  void* cached_lse;           /* optional [B, Hq] */
+  int32_t* fallbacks;         /* optional [B, Hq]: 1 when remove() fell back to the split prefix */
+  /* ---- scratch --------------------------------------------------------- */
+  void* workspace;
+  size_t workspace_bytes;
+} MacDecodeParams;
+
+/* Per-shard (acc, lse) partial merge for the KV-sharded miss path. */
+typedef struct MacMergeParams {
+  int32_t n_parts;       /* G partials per row */
+  int32_t n_rows;        /* rows (request x head) */
+  int32_t head_dim_v;
+  int32_t dtype;         /* MAC_DT_F32 | MAC_DT_F64 */
+  const void* part_acc;  /* [G, n_rows, d_v] normalised acc */
+  const void* part_lse;  /* [G, n_rows] lse (-inf: empty) */
+  void* out_acc;         /* [n_rows, d_v] */
+  void* out_lse;         /* [n_rows] */
+} MacMergeParams;
+
+int mac_abi_version(void);
+size_t mac_params_size(void);
+const char* mac_error_string(int code);
+/* bytes of scratch the decode entry points need for this geometry */
+size_t mac_workspace_bytes(const MacDecodeParams* p);
+/* which kernel family mac_amend would launch: 0 generic CUDA-core, 1 bf16 tensor-core (mma) */
+int mac_amend_variant(const MacDecodeParams* p);
+
+int mac_append_kv(const MacDecodeParams* p, void* stream);
+int mac_match(const MacDecodeParams* p, void* stream);
+int mac_amend(const MacDecodeParams* p, void* stream);
+int mac_complete(const MacDecodeParams* p, void* stream);
+int mac_decode_step(const MacDecodeParams* p, void* stream);
+int mac_full_decode(const MacDecodeParams* p, void* stream);
+int mac_attend_full(const MacDecodeParams* p, void* stream);
+int mac_merge_partials(const MacMergeParams* p, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MACATTN_H_ */

@@ -1,0 +1,57 @@
+"""B200-native MAC-Attention decode path (match -> amend -> complete, full-attention fallback).
+
+Drop-in for the decode path of the reference package `attnreuse`: the same
+public names for the engine, its configuration and result types, the metrics
+and the trace format, backed by hand-written sm_100a CUDA kernels behind the
+C-ABI library `lib/libmacattn.so` (include/macattn.h).  There is no CPU path:
+decode calls fail loudly when the library or a CUDA device is missing.
+"""
+
+from .config import (
+    DOWNDATE_REMOVE,
+    DOWNDATE_SPLIT,
+    MATCH_POST_ROPE,
+    MATCH_PRE_ROPE,
+    AttentionSummary,
+    ByteCostModel,
+    CancellationError,
+    DecodeMetrics,
+    EmptySummaryError,
+    EngineConfig,
+    MassExceededError,
+    MatchConfig,
+    MatchResult,
+    StepResult,
+    aux_overhead_ratio,
+    aux_overhead_rule_of_thumb,
+    break_even_gate,
+    compute_metrics,
+    empty_summary,
+    fidelity_efficiency,
+    finalize,
+    group_kv_span,
+    threshold,
+)
+from .workload import PRESETS, SyntheticSpec, Trace, TraceError, gen_synthetic, read_trace, write_trace
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # the device engines import torch; load them on first use
+    if name in ("BatchDecodeEngine", "BatchStepResult", "DecodeEngine", "run_decode", "KvStoreView",
+                "QueryRingView", "SummaryRingView", "TrafficCounter", "rope_freqs"):
+        from . import engine
+
+        return getattr(engine, name)
+    raise AttributeError(name)
+
+
+__all__ = [
+    "AttentionSummary", "BatchDecodeEngine", "BatchStepResult", "ByteCostModel", "CancellationError",
+    "DOWNDATE_REMOVE", "DOWNDATE_SPLIT", "DecodeEngine", "DecodeMetrics", "EmptySummaryError", "EngineConfig",
+    "MATCH_POST_ROPE", "MATCH_PRE_ROPE", "MassExceededError", "MatchConfig", "MatchResult", "PRESETS",
+    "StepResult", "SyntheticSpec", "Trace", "TraceError", "TrafficCounter", "aux_overhead_ratio",
+    "aux_overhead_rule_of_thumb", "break_even_gate", "compute_metrics", "empty_summary", "fidelity_efficiency",
+    "finalize", "gen_synthetic", "group_kv_span", "read_trace", "run_decode", "threshold", "write_trace",
+]

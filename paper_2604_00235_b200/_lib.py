@@ -1,0 +1,154 @@
+"""ctypes binding of the C-ABI library lib/libmacattn.so (include/macattn.h).
+
+This is the ONLY way the product reaches compute: there is no CPU or
+PyTorch fallback.  A missing or stale library raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmacattn.so")
+
+ABI_VERSION = 1
+
+MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
+DT_F32, DT_BF16, DT_F64 = 0, 1, 2
+MATCH_PRE_ROPE, MATCH_POST_ROPE = 0, 1
+DOWNDATE_SPLIT, DOWNDATE_REMOVE = 0, 1
+
+EXPORTS = (
+    "mac_abi_version",
+    "mac_params_size",
+    "mac_error_string",
+    "mac_workspace_bytes",
+    "mac_amend_variant",
+    "mac_append_kv",
+    "mac_match",
+    "mac_amend",
+    "mac_complete",
+    "mac_decode_step",
+    "mac_full_decode",
+    "mac_attend_full",
+    "mac_merge_partials",
+)
+
+
+class MacDecodeParams(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32),
+        ("n_q_heads", C.c_int32),
+        ("n_kv_heads", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("head_dim_v", C.c_int32),
+        ("window", C.c_int32),
+        ("band", C.c_int32),
+        ("page_size", C.c_int32),
+        ("pages_per_seq", C.c_int32),
+        ("storage", C.c_int32),
+        ("in_dtype", C.c_int32),
+        ("max_chunks", C.c_int32),
+        ("min_chunk", C.c_int32),
+        ("kv_offset", C.c_int32),
+        ("thr_sq", C.c_double),
+        ("delta_max", C.c_int32),
+        ("match_space", C.c_int32),
+        ("refresh_every", C.c_int32),
+        ("roi_gate", C.c_int32),
+        ("roi_b_kv", C.c_double),
+        ("roi_b_q", C.c_double),
+        ("downdate", C.c_int32),
+        ("force_miss", C.c_int32),
+        ("eps_cancel", C.c_double),
+        ("seq_lens", C.c_void_p),
+        ("page_table", C.c_void_p),
+        ("k_cache", C.c_void_p),
+        ("v_cache", C.c_void_p),
+        ("ring_q", C.c_void_p),
+        ("ring_acc", C.c_void_p),
+        ("ring_lse", C.c_void_p),
+        ("rope_freqs", C.c_void_p),
+        ("q_pre", C.c_void_p),
+        ("k_pre", C.c_void_p),
+        ("v_in", C.c_void_p),
+        ("out", C.c_void_p),
+        ("match_hit", C.c_void_p),
+        ("use_hit", C.c_void_p),
+        ("match_pos", C.c_void_p),
+        ("match_dist", C.c_void_p),
+        ("match_scanned", C.c_void_p),
+        ("full_lse", C.c_void_p),
+        ("band_mass", C.c_void_p),
+        ("cached_acc", C.c_void_p),
+        ("cached_lse", C.c_void_p),
+        ("fallbacks", C.c_void_p),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_size_t),
+    ]
+
+
+class MacMergeParams(C.Structure):
+    _fields_ = [
+        ("n_parts", C.c_int32),
+        ("n_rows", C.c_int32),
+        ("head_dim_v", C.c_int32),
+        ("dtype", C.c_int32),
+        ("part_acc", C.c_void_p),
+        ("part_lse", C.c_void_p),
+        ("out_acc", C.c_void_p),
+        ("out_lse", C.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load and check the library once; raise loudly if it is absent or mismatched."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"macattn CUDA library not found at {LIB_PATH}; build it with "
+            "`python -m paper_2604_00235_b200.build` (there is no CPU fallback)"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name in EXPORTS:
+        if not hasattr(lib, name):
+            raise RuntimeError(f"{LIB_PATH} does not export {name}")
+    lib.mac_abi_version.restype = C.c_int
+    lib.mac_params_size.restype = C.c_size_t
+    lib.mac_error_string.restype = C.c_char_p
+    lib.mac_error_string.argtypes = [C.c_int]
+    lib.mac_workspace_bytes.restype = C.c_size_t
+    lib.mac_workspace_bytes.argtypes = [C.POINTER(MacDecodeParams)]
+    lib.mac_amend_variant.restype = C.c_int
+    lib.mac_amend_variant.argtypes = [C.POINTER(MacDecodeParams)]
+    for name in ("mac_append_kv", "mac_match", "mac_amend", "mac_complete", "mac_decode_step", "mac_full_decode",
+                 "mac_attend_full"):
+        fn = getattr(lib, name)
+        fn.restype = C.c_int
+        fn.argtypes = [C.POINTER(MacDecodeParams), C.c_void_p]
+    lib.mac_merge_partials.restype = C.c_int
+    lib.mac_merge_partials.argtypes = [C.POINTER(MacMergeParams), C.c_void_p]
+    if lib.mac_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"libmacattn ABI {lib.mac_abi_version()} != expected {ABI_VERSION}; rebuild")
+    if lib.mac_params_size() != C.sizeof(MacDecodeParams):
+        raise RuntimeError("libmacattn MacDecodeParams layout differs from the ctypes mirror; rebuild")
+    _lib = lib
+    return lib
+
+
+def check(code: int, what: str):
+    if code != 0:
+        msg = load().mac_error_string(code).decode()
+        raise RuntimeError(f"{what} failed ({code}): {msg}")
+
+
+def call(name: str, params, stream_handle: int):
+    lib = load()
+    code = getattr(lib, name)(C.byref(params), C.c_void_p(stream_handle))
+    check(code, name)

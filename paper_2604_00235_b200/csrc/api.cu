@@ -1,0 +1,127 @@
+// C-ABI entry points (include/macattn.h): validation, dispatch, step sequencing.
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace mac {
+template <int MODE> cudaError_t launch_append(const MacDecodeParams&, cudaStream_t, int);
+template <int MODE> cudaError_t launch_match_generic(const MacDecodeParams&, cudaStream_t);
+template <int MODE> cudaError_t launch_amend_generic(const MacDecodeParams&, cudaStream_t);
+template <int MODE> cudaError_t launch_complete(const MacDecodeParams&, cudaStream_t, int);
+cudaError_t launch_match_bf16_d128(const MacDecodeParams&, cudaStream_t);
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t);
+bool amend_mma_supported(const MacDecodeParams&);
+bool match_fast_supported(const MacDecodeParams&);
+cudaError_t launch_merge_partials(const MacMergeParams&, cudaStream_t);
+}  // namespace mac
+
+using namespace mac;
+
+static int validate(const MacDecodeParams* p, bool need_ring) {
+  if (!p) return MAC_ERR_NULL;
+  if (p->batch < 1 || p->n_q_heads < 1 || p->n_kv_heads < 1 || p->n_q_heads % p->n_kv_heads) return MAC_ERR_SHAPE;
+  if (p->head_dim < 2 || p->head_dim % 2 || p->head_dim > 1024 || p->head_dim_v < 1 || p->head_dim_v > 1024)
+    return MAC_ERR_SHAPE;
+  if (p->n_q_heads / p->n_kv_heads > 64) return MAC_ERR_SHAPE;
+  if (p->window < 1 || p->band < 0 || p->max_chunks < 1 || p->min_chunk < 1 || p->kv_offset < 0) return MAC_ERR_SHAPE;
+  if (p->storage < MAC_MODE_F32 || p->storage > MAC_MODE_F64) return MAC_ERR_DTYPE;
+  if (p->in_dtype < MAC_DT_F32 || p->in_dtype > MAC_DT_F64) return MAC_ERR_DTYPE;
+  if (p->page_size < 1 || p->pages_per_seq < 1) return MAC_ERR_PAGING;
+  if (!p->seq_lens || !p->page_table || !p->k_cache || !p->v_cache || !p->rope_freqs || !p->q_pre || !p->k_pre ||
+      !p->v_in || !p->out || !p->full_lse || !p->workspace)
+    return MAC_ERR_NULL;
+  if (need_ring && (!p->ring_q || !p->ring_acc || !p->ring_lse || !p->match_hit || !p->use_hit || !p->match_pos ||
+                    !p->match_dist || !p->match_scanned || !p->band_mass))
+    return MAC_ERR_NULL;
+  if (p->workspace_bytes < workspace_layout(*p).total) return MAC_ERR_WORKSPACE;
+  return MAC_OK;
+}
+
+template <int MODE>
+static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int stage_mask) {
+  cudaError_t e = cudaSuccess;
+  if (stage_mask & 1) { e = launch_append<MODE>(p, st, 0); if (e) return e; }
+  if (stage_mask & 32) { e = launch_append<MODE>(p, st, 1); if (e) return e; }
+  if (stage_mask & 2) {
+    if (MODE == MAC_MODE_BF16 && match_fast_supported(p)) e = launch_match_bf16_d128(p, st);
+    else e = launch_match_generic<MODE>(p, st);
+    if (e) return e;
+  }
+  if (stage_mask & 4) {
+    if (MODE == MAC_MODE_BF16 && amend_mma_supported(p)) e = launch_amend_mma_bf16(p, st);
+    else e = launch_amend_generic<MODE>(p, st);
+    if (e) return e;
+  }
+  if (stage_mask & 8) { e = launch_complete<MODE>(p, st, 0); if (e) return e; }
+  if (stage_mask & 16) { e = launch_complete<MODE>(p, st, 1); if (e) return e; }
+  return e;
+}
+
+static int dispatch(const MacDecodeParams* p, void* stream, int stage_mask, bool need_ring) {
+  int v = validate(p, need_ring);
+  if (v) return v;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (p->storage) {
+    case MAC_MODE_F32: e = run_step<MAC_MODE_F32>(*p, st, stage_mask); break;
+    case MAC_MODE_BF16: e = run_step<MAC_MODE_BF16>(*p, st, stage_mask); break;
+    default: e = run_step<MAC_MODE_F64>(*p, st, stage_mask); break;
+  }
+  return (int)e;
+}
+
+extern "C" {
+
+int mac_abi_version(void) { return MACATTN_ABI_VERSION; }
+size_t mac_params_size(void) { return sizeof(MacDecodeParams); }
+
+const char* mac_error_string(int code) {
+  switch (code) {
+    case MAC_OK: return "ok";
+    case MAC_ERR_NULL: return "macattn: a required pointer is NULL";
+    case MAC_ERR_SHAPE: return "macattn: head counts / dims / window / band out of range";
+    case MAC_ERR_DTYPE: return "macattn: unknown storage mode or input dtype";
+    case MAC_ERR_WORKSPACE: return "macattn: workspace smaller than mac_workspace_bytes()";
+    case MAC_ERR_PAGING: return "macattn: invalid page geometry";
+    default: return cudaGetErrorString((cudaError_t)code);
+  }
+}
+
+size_t mac_workspace_bytes(const MacDecodeParams* p) { return p ? workspace_layout(*p).total : 0; }
+
+int mac_amend_variant(const MacDecodeParams* p) {
+  return (p && p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) ? 1 : 0;
+}
+
+int mac_append_kv(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 1, false); }
+int mac_match(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 2, true); }
+int mac_amend(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 4, true); }
+int mac_complete(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 8, true); }
+int mac_decode_step(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 1 | 2 | 4 | 8, true); }
+
+int mac_full_decode(const MacDecodeParams* p, void* stream) {
+  if (!p) return MAC_ERR_NULL;
+  MacDecodeParams q = *p;
+  q.force_miss = 1;
+  q.band = 0;  // no prefix/band split: one summary over [1, m]
+  return dispatch(&q, stream, 1 | 4 | 16, false);
+}
+
+int mac_attend_full(const MacDecodeParams* p, void* stream) {
+  if (!p) return MAC_ERR_NULL;
+  MacDecodeParams q = *p;
+  q.force_miss = 1;
+  q.band = 0;
+  return dispatch(&q, stream, 32 | 4 | 16, false);
+}
+
+int mac_merge_partials(const MacMergeParams* p, void* stream) {
+  if (!p) return MAC_ERR_NULL;
+  if (p->n_parts < 1 || p->n_rows < 1 || p->head_dim_v < 1) return MAC_ERR_SHAPE;
+  if (p->dtype != MAC_DT_F32 && p->dtype != MAC_DT_F64) return MAC_ERR_DTYPE;
+  if (!p->part_acc || !p->part_lse || !p->out_acc || !p->out_lse) return MAC_ERR_NULL;
+  return (int)launch_merge_partials(*p, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,522 @@
+"""Decode engines: the batched device engine and the reference-shaped shim.
+
+`BatchDecodeEngine` is the B200 serving form of the path: all state (paged
+KV cache, per-(request, head) query ring and summary ring, sequence lengths)
+lives in HBM as batched tensors, and one `decode_step(layer, ...)` is four
+stream-ordered kernel launches through the C-ABI library (append+RoPE,
+match, amend, complete) with no host synchronisation.
+
+`DecodeEngine` keeps the reference's single-request API (engine.py:334-539):
+`decode_step(layer, q_pre, k_pre, v, m, oracle_rows=None) -> StepResult`
+with host numpy in and out, the same exceptions, metrics and ring views.
+It runs the very same device kernels (B = 1) and copies results back.
+
+Data layout in HBM (per layer):
+  k_cache, v_cache  [num_pages, Hkv, page_size, d]   post-RoPE keys / values (storage dtype)
+  ring_q            [B, Hq, W, d]                    pre-RoPE queries, slot (pos-1) % W
+  ring_acc          [B, Hq, W, d_v]  f32 (f64)       prefix summary acc over [1, max(0, pos-r)]
+  ring_lse          [B, Hq, W]       f32 (f64)       prefix summary lse, -inf = empty
+  seq_lens          [B] int32                        tokens stored
+and per engine: page_table [B, pages_per_seq] int32 shared by all layers.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import (
+    DOWNDATE_REMOVE,
+    MATCH_POST_ROPE,
+    AttentionSummary,
+    DecodeMetrics,
+    EngineConfig,
+    MatchResult,
+    StepResult,
+    threshold,
+)
+
+_TORCH_STORAGE = {"f32": torch.float32, "bf16": torch.bfloat16, "f64": torch.float64}
+_MODE = {"f32": _lib.MODE_F32, "bf16": _lib.MODE_BF16, "f64": _lib.MODE_F64}
+_IN_DT = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16, torch.float64: _lib.DT_F64}
+
+SM_COUNT_B200 = 148
+
+
+def rope_freqs(d: int, base: float) -> np.ndarray:
+    """omega_j = base**(-2j/d) evaluated exactly as attention.py:208-209 (numpy f64)."""
+    j = np.arange(d // 2, dtype=np.float64)
+    return base ** (-2.0 * j / d)
+
+
+def default_max_chunks(batch: int, n_kv_heads: int) -> int:
+    """Split-KV slots per (request, kv head): enough items for ~8 per SM when every head misses."""
+    groups = batch * n_kv_heads
+    return int(min(1024, max(8, math.ceil(SM_COUNT_B200 * 8 / groups))))
+
+
+@dataclass
+class BatchStepResult:
+    """Device tensors of one batched step (views of engine-owned buffers; valid until the next step)."""
+
+    out: torch.Tensor          # [B, Hq, d_v]
+    match_hit: torch.Tensor    # [B, Hq] int32, raw decision
+    use_hit: torch.Tensor      # [B, Hq] int32, after gates
+    match_pos: torch.Tensor    # [B, Hq] int32, -1 on raw miss
+    match_dist: torch.Tensor   # [B, Hq] f64
+    match_scanned: torch.Tensor
+    full_lse: torch.Tensor
+    band_mass: torch.Tensor
+    cached_acc: torch.Tensor | None
+    cached_lse: torch.Tensor | None
+    fallbacks: torch.Tensor
+
+
+class BatchDecodeEngine:
+    """Batched MAC decode state on one GPU; B independent requests, n_layers layers."""
+
+    def __init__(self, cfg: EngineConfig, batch: int, max_seq_len: int, *, device="cuda",
+                 max_chunks: int | None = None, min_chunk: int = 256, page_perm_seed: int | None = None,
+                 record_cached: bool = False, kv_offset: int = 0):
+        if batch < 1:
+            raise ValueError("batch must be >= 1")
+        if max_seq_len < 1:
+            raise ValueError("max_seq_len must be >= 1")
+        _lib.load()
+        self.cfg = cfg
+        self.batch = batch
+        self.device = torch.device(device)
+        self.sdt = _TORCH_STORAGE[cfg.storage]
+        self.sumdt = torch.float64 if cfg.storage == "f64" else torch.float32
+        self.group = cfg.n_q_heads // cfg.n_kv_heads
+        self.page_size = cfg.page_size
+        self.max_chunks = max_chunks or default_max_chunks(batch, cfg.n_kv_heads)
+        self.min_chunk = min_chunk
+        self.kv_offset = kv_offset
+        self.record_cached = record_cached
+        self._page_perm_seed = page_perm_seed
+        dev = self.device
+        self.freqs = torch.from_numpy(rope_freqs(cfg.d, cfg.rope_base)).to(dev)
+        self.capacity = 0
+        self.k_cache: list[torch.Tensor] = []
+        self.v_cache: list[torch.Tensor] = []
+        self.page_table = None
+        self._alloc_kv(max_seq_len)
+        B, Hq, W, d, dv = batch, cfg.n_q_heads, cfg.window, cfg.d, cfg.d_v
+        L = cfg.n_layers
+        self.ring_q = [torch.zeros(B, Hq, W, d, dtype=self.sdt, device=dev) for _ in range(L)]
+        self.ring_acc = [torch.zeros(B, Hq, W, dv, dtype=self.sumdt, device=dev) for _ in range(L)]
+        self.ring_lse = [torch.full((B, Hq, W), -math.inf, dtype=self.sumdt, device=dev) for _ in range(L)]
+        self.seq_lens = [torch.zeros(B, dtype=torch.int32, device=dev) for _ in range(L)]
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.o_out = torch.empty(B, Hq, dv, dtype=self.sumdt, device=dev)
+        self.o_hit = torch.zeros(B, Hq, **i32)
+        self.o_use = torch.zeros(B, Hq, **i32)
+        self.o_pos = torch.full((B, Hq), -1, **i32)
+        self.o_dist = torch.zeros(B, Hq, dtype=torch.float64, device=dev)
+        self.o_scanned = torch.zeros(B, Hq, **i32)
+        self.o_full_lse = torch.zeros(B, Hq, dtype=self.sumdt, device=dev)
+        self.o_band_mass = torch.zeros(B, Hq, dtype=self.sumdt, device=dev)
+        self.o_fallbacks = torch.zeros(B, Hq, **i32)
+        self.o_cached_acc = torch.zeros(B, Hq, dv, dtype=self.sumdt, device=dev) if record_cached else None
+        self.o_cached_lse = torch.zeros(B, Hq, dtype=self.sumdt, device=dev) if record_cached else None
+        probe = self._params(0, self.o_out, self.o_out, self.o_out, _lib.DT_F32)
+        self.workspace = torch.empty(int(_lib.load().mac_workspace_bytes(probe)), dtype=torch.uint8, device=dev)
+
+    # ------------------------------------------------------------------ memory
+    def _alloc_kv(self, tokens: int):
+        cfg, B, ps = self.cfg, self.batch, self.page_size
+        pps = -(-tokens // ps)
+        n_pages = B * pps
+        dev = self.device
+        if self._page_perm_seed is not None:
+            g = torch.Generator().manual_seed(self._page_perm_seed)
+            ids = torch.randperm(n_pages, generator=g).to(torch.int32)
+        else:
+            ids = torch.arange(n_pages, dtype=torch.int32)
+        table = ids.view(B, pps).to(dev)
+        new_k, new_v = [], []
+        for layer in range(cfg.n_layers):
+            k = torch.zeros(n_pages, cfg.n_kv_heads, ps, cfg.d, dtype=self.sdt, device=dev)
+            v = torch.zeros(n_pages, cfg.n_kv_heads, ps, cfg.d_v, dtype=self.sdt, device=dev)
+            if self.page_table is not None:
+                old_pps = self.page_table.shape[1]
+                src = self.page_table.long()
+                dst = table[:, :old_pps].long()
+                k[dst.reshape(-1)] = self.k_cache[layer][src.reshape(-1)]
+                v[dst.reshape(-1)] = self.v_cache[layer][src.reshape(-1)]
+            new_k.append(k)
+            new_v.append(v)
+        self.k_cache, self.v_cache, self.page_table = new_k, new_v, table
+        self.capacity = pps * ps
+
+    def reserve(self, tokens: int):
+        """Grow the paged KV pool so every request can hold `tokens` tokens (doubling)."""
+        if tokens > self.capacity:
+            self._alloc_kv(max(tokens, 2 * self.capacity))
+
+    # ------------------------------------------------------------------ launch
+    def _params(self, layer: int, q, k, v, in_dt: int, force_miss: bool = False) -> _lib.MacDecodeParams:
+        cfg = self.cfg
+        P = _lib.MacDecodeParams()
+        P.batch = self.batch
+        P.n_q_heads, P.n_kv_heads = cfg.n_q_heads, cfg.n_kv_heads
+        P.head_dim, P.head_dim_v = cfg.d, cfg.d_v
+        P.window, P.band = cfg.window, cfg.band
+        P.page_size = self.page_size
+        P.pages_per_seq = self.page_table.shape[1]
+        P.storage = _MODE[cfg.storage]
+        P.in_dtype = in_dt
+        P.max_chunks, P.min_chunk = self.max_chunks, self.min_chunk
+        P.kv_offset = self.kv_offset
+        P.thr_sq = threshold(cfg.d, cfg.tau_for(layer)) ** 2
+        P.delta_max = cfg.delta_max or 0
+        P.match_space = _lib.MATCH_POST_ROPE if cfg.match_space == MATCH_POST_ROPE else _lib.MATCH_PRE_ROPE
+        P.refresh_every = cfg.refresh_every
+        costs = cfg.byte_costs()
+        P.roi_gate = int(cfg.roi_gate)
+        P.roi_b_kv, P.roi_b_q = float(costs.b_kv), float(costs.b_q)
+        P.downdate = _lib.DOWNDATE_REMOVE if cfg.downdate_mode == DOWNDATE_REMOVE else _lib.DOWNDATE_SPLIT
+        P.force_miss = int(force_miss)
+        P.eps_cancel = 1e-6
+        P.seq_lens = self.seq_lens[layer].data_ptr()
+        P.page_table = self.page_table.data_ptr()
+        P.k_cache, P.v_cache = self.k_cache[layer].data_ptr(), self.v_cache[layer].data_ptr()
+        P.ring_q = self.ring_q[layer].data_ptr()
+        P.ring_acc = self.ring_acc[layer].data_ptr()
+        P.ring_lse = self.ring_lse[layer].data_ptr()
+        P.rope_freqs = self.freqs.data_ptr()
+        P.q_pre, P.k_pre, P.v_in = q.data_ptr(), k.data_ptr(), v.data_ptr()
+        P.out = self.o_out.data_ptr()
+        P.match_hit, P.use_hit = self.o_hit.data_ptr(), self.o_use.data_ptr()
+        P.match_pos, P.match_dist = self.o_pos.data_ptr(), self.o_dist.data_ptr()
+        P.match_scanned = self.o_scanned.data_ptr()
+        P.full_lse, P.band_mass = self.o_full_lse.data_ptr(), self.o_band_mass.data_ptr()
+        P.cached_acc = self.o_cached_acc.data_ptr() if self.o_cached_acc is not None else None
+        P.cached_lse = self.o_cached_lse.data_ptr() if self.o_cached_lse is not None else None
+        P.fallbacks = self.o_fallbacks.data_ptr()
+        if hasattr(self, "workspace"):
+            P.workspace = self.workspace.data_ptr()
+            P.workspace_bytes = self.workspace.numel()
+        else:
+            P.workspace = 1
+            P.workspace_bytes = 0
+        return P
+
+    def _check_inputs(self, q, k, v):
+        cfg, B = self.cfg, self.batch
+        if tuple(q.shape) != (B, cfg.n_q_heads, cfg.d):
+            raise ValueError(f"expected queries {(B, cfg.n_q_heads, cfg.d)}, got {tuple(q.shape)}")
+        if tuple(k.shape) != (B, cfg.n_kv_heads, cfg.d) or tuple(v.shape) != (B, cfg.n_kv_heads, cfg.d_v):
+            raise ValueError("key/value shapes do not match the configured kv heads")
+        if not (q.dtype == k.dtype == v.dtype) or q.dtype not in _IN_DT:
+            raise ValueError("q_pre, k_pre and v must share one dtype among float32/bfloat16/float64")
+        for t in (q, k, v):
+            if t.device != self.device and not (t.is_cuda and self.device.type == "cuda"):
+                raise ValueError("inputs must live on the engine's device")
+            if not t.is_contiguous():
+                raise ValueError("inputs must be contiguous")
+        return _IN_DT[q.dtype]
+
+    def _layer(self, layer: int):
+        if not 0 <= layer < self.cfg.n_layers:
+            raise ValueError(f"layer {layer} out of range")
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def decode_step(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor) -> BatchStepResult:
+        """One MAC step for every request: append -> match -> amend -> complete (engine.py:410-539)."""
+        self._layer(layer)
+        dt = self._check_inputs(q_pre, k_pre, v)
+        _lib.call("mac_decode_step", self._params(layer, q_pre, k_pre, v, dt), self._stream())
+        return self.result()
+
+    def stage(self, name: str, layer: int, q_pre, k_pre, v, force_miss: bool = False):
+        """Launch one stage (mac_append_kv | mac_match | mac_amend | mac_complete) — for profiling/tests."""
+        self._layer(layer)
+        dt = self._check_inputs(q_pre, k_pre, v)
+        _lib.call(name, self._params(layer, q_pre, k_pre, v, dt, force_miss), self._stream())
+
+    def full_decode(self, layer: int, q_pre, k_pre, v) -> torch.Tensor:
+        """Full-attention decode (append + exact attention over [1, m]): the baseline; no ring work."""
+        self._layer(layer)
+        dt = self._check_inputs(q_pre, k_pre, v)
+        _lib.call("mac_full_decode", self._params(layer, q_pre, k_pre, v, dt, True), self._stream())
+        return self.o_out
+
+    def attend_full(self, layer: int, q_pre) -> torch.Tensor:
+        """Exact attention of R_m q over the stored [1, m] (m = seq_lens), without appending."""
+        self._layer(layer)
+        cfg = self.cfg
+        dt = _IN_DT[q_pre.dtype]
+        kv_dummy_k = torch.empty(self.batch, cfg.n_kv_heads, cfg.d, dtype=q_pre.dtype, device=self.device)
+        kv_dummy_v = torch.empty(self.batch, cfg.n_kv_heads, cfg.d_v, dtype=q_pre.dtype, device=self.device)
+        _lib.call("mac_attend_full", self._params(layer, q_pre, kv_dummy_k, kv_dummy_v, dt, True), self._stream())
+        return self.o_out
+
+    def result(self) -> BatchStepResult:
+        return BatchStepResult(self.o_out, self.o_hit, self.o_use, self.o_pos, self.o_dist, self.o_scanned,
+                               self.o_full_lse, self.o_band_mass, self.o_cached_acc, self.o_cached_lse,
+                               self.o_fallbacks)
+
+    # ------------------------------------------------------------------ state injection
+    def inject(self, layer: int, k_rot: torch.Tensor, v: torch.Tensor, ring_q: torch.Tensor, ring_acc: torch.Tensor,
+               ring_lse: torch.Tensor, n: int):
+        """Load a prefix state for every request: K/V rows 1..n (post-RoPE, [B, Hkv, n, d]) and the
+        ring entries of positions n-cnt+1..n ([B, Hq, cnt, ...], cnt = min(n, W), oldest first)."""
+        cfg, B, ps = self.cfg, self.batch, self.page_size
+        self.reserve(n + 1)
+        pages = -(-n // ps)
+        for b in range(B):
+            ids = self.page_table[b, :pages].long()
+            kk = torch.zeros(pages * ps, cfg.n_kv_heads, cfg.d, dtype=self.sdt, device=self.device)
+            vv = torch.zeros(pages * ps, cfg.n_kv_heads, cfg.d_v, dtype=self.sdt, device=self.device)
+            kk[:n] = k_rot[b].transpose(0, 1).to(self.sdt)
+            vv[:n] = v[b].transpose(0, 1).to(self.sdt)
+            self.k_cache[layer][ids] = kk.view(pages, ps, cfg.n_kv_heads, cfg.d).transpose(1, 2)
+            self.v_cache[layer][ids] = vv.view(pages, ps, cfg.n_kv_heads, cfg.d_v).transpose(1, 2)
+        cnt = ring_q.shape[2]
+        W = cfg.window
+        pos = torch.arange(n - cnt + 1, n + 1, device=self.device)
+        slots = (pos - 1) % W
+        self.ring_q[layer][:, :, slots] = ring_q.to(self.sdt)
+        self.ring_acc[layer][:, :, slots] = ring_acc.to(self.sumdt)
+        self.ring_lse[layer][:, :, slots] = ring_lse.to(self.sumdt)
+        self.seq_lens[layer].fill_(n)
+
+
+# ----------------------------------------------------------------------------
+# reference-shaped single-request shim
+# ----------------------------------------------------------------------------
+
+class QueryRingView:
+    """Read-only view of one (layer, head) query ring (matching.py:67-126)."""
+
+    def __init__(self, eng: "DecodeEngine", layer: int, head: int):
+        self._e, self._l, self._h = eng, layer, head
+        self.capacity = eng.cfg.window
+        self.d = eng.cfg.d
+
+    def _count(self) -> int:
+        return int(self._e._n[self._l])
+
+    def __len__(self):
+        return min(self._count(), self.capacity)
+
+    @property
+    def last_position(self) -> int:
+        return self._count()
+
+    def _positions(self) -> np.ndarray:
+        n, W = self._count(), self.capacity
+        slots = np.arange(len(self))
+        # latest position p <= n with (p - 1) % W == slot
+        return n - ((n - 1 - slots) % W)
+
+    def view(self):
+        n = len(self)
+        q = self._e.batch.ring_q[self._l][0, self._h, :n].double().cpu().numpy()
+        return q, np.einsum("ij,ij->i", q, q), self._positions()
+
+    def slot_of(self, pos: int) -> int:
+        slot = (pos - 1) % self.capacity
+        n = len(self)
+        if n == 0 or slot >= n or int(self._positions()[slot]) != pos:
+            raise KeyError(f"position {pos} is not in the ring")
+        return slot
+
+    def query_at(self, pos: int) -> np.ndarray:
+        return self._e.batch.ring_q[self._l][0, self._h, self.slot_of(pos)].double().cpu().numpy()
+
+
+class SummaryRingView:
+    """Read-only view of one (layer, head) summary ring (engine.py:284-320)."""
+
+    def __init__(self, eng: "DecodeEngine", layer: int, head: int):
+        self._q = QueryRingView(eng, layer, head)
+        self._e, self._l, self._h = eng, layer, head
+        self.capacity = eng.cfg.window
+
+    def __len__(self):
+        return len(self._q)
+
+    @property
+    def last_position(self) -> int:
+        return self._q.last_position
+
+    def summary_at(self, pos: int) -> AttentionSummary:
+        slot = self._q.slot_of(pos)
+        b = self._e.batch
+        acc = b.ring_acc[self._l][0, self._h, slot].double().cpu().numpy()
+        lse = float(b.ring_lse[self._l][0, self._h, slot].item())
+        return AttentionSummary(acc=acc, lse=lse, count=max(0, pos - self._e.cfg.band))
+
+
+class TrafficCounter:
+    """Logical KV read traffic (kvstore.py:19-30), folded from the device decisions."""
+
+    def __init__(self):
+        from collections import Counter
+
+        self.tokens_read = 0
+        self.bytes_read = 0
+        self.read_histogram = Counter()
+
+    def record(self, tokens: int, nbytes: int):
+        self.tokens_read += tokens
+        self.bytes_read += nbytes
+        self.read_histogram[tokens.bit_length()] += 1
+
+
+class KvStoreView:
+    """Host view of the paged device KV cache with the KvStore read API (kvstore.py:62-165)."""
+
+    def __init__(self, eng: "DecodeEngine"):
+        self._e = eng
+        self.d, self.d_v, self.page_size = eng.cfg.d, eng.cfg.d_v, eng.cfg.page_size
+
+    @property
+    def token_bytes(self) -> int:
+        return (self.d + self.d_v) * self._e.cfg.storage_itemsize
+
+    def length(self, layer: int, kv_head: int) -> int:
+        return int(self._e._n[layer])
+
+    def read_range(self, layer: int, kv_head: int, span, counter=None):
+        lo, hi = span
+        n = self.length(layer, kv_head)
+        if lo < 1 or hi < lo:
+            raise ValueError(f"invalid token range [{lo}, {hi}]")
+        if hi > n:
+            raise ValueError(f"token range [{lo}, {hi}] exceeds stored length {n}")
+        b = self._e.batch
+        idx = torch.arange(lo - 1, hi, device=b.device)
+        pages = b.page_table[0, idx // b.page_size].long()
+        slots = idx % b.page_size
+        keys = b.k_cache[layer][pages, kv_head, slots].double().cpu().numpy()
+        vals = b.v_cache[layer][pages, kv_head, slots].double().cpu().numpy()
+        if counter is not None:
+            counter.record(hi - lo + 1, (hi - lo + 1) * self.token_bytes)
+        return keys, vals
+
+    def n_pages(self, layer: int, kv_head: int) -> int:
+        return -(-self.length(layer, kv_head) // self.page_size)
+
+
+class DecodeEngine:
+    """Single-request decoder with the reference API (engine.py:334-539) on the CUDA path."""
+
+    def __init__(self, cfg: EngineConfig, *, device="cuda", capacity: int = 1024):
+        self.cfg = cfg
+        self.batch = BatchDecodeEngine(cfg, 1, max(capacity, 16), device=device, record_cached=True)
+        self.device = self.batch.device
+        self.costs = cfg.byte_costs()
+        self.metrics = DecodeMetrics()
+        self.traffic = TrafficCounter()
+        self.oracle_traffic = TrafficCounter()
+        self.store = KvStoreView(self)
+        self._n = [0] * cfg.n_layers
+        self._group = cfg.n_q_heads // cfg.n_kv_heads
+
+    def rings(self, layer: int, head: int):
+        return QueryRingView(self, layer, head), SummaryRingView(self, layer, head)
+
+    def decode_step(self, layer: int, q_pre, k_pre, v, m: int, oracle_rows=None) -> StepResult:
+        cfg = self.cfg
+        r = cfg.band
+        q_pre = np.asarray(q_pre, dtype=np.float64)
+        k_pre = np.asarray(k_pre, dtype=np.float64)
+        v = np.asarray(v, dtype=np.float64)
+        if q_pre.shape != (cfg.n_q_heads, cfg.d):
+            raise ValueError(f"expected queries ({cfg.n_q_heads}, {cfg.d}), got {q_pre.shape}")
+        if k_pre.shape != (cfg.n_kv_heads, cfg.d) or v.shape != (cfg.n_kv_heads, cfg.d_v):
+            raise ValueError("key/value shapes do not match the configured kv heads")
+        if not 0 <= layer < cfg.n_layers:
+            raise ValueError(f"layer {layer} out of range")
+        if m != self._n[layer] + 1:
+            raise ValueError(f"steps must be consecutive: store is at {self._n[layer] + 1}, step is {m}")
+        self.batch.reserve(m)
+        dev = self.device
+        q = torch.from_numpy(q_pre).to(dev)[None].contiguous()
+        k = torch.from_numpy(k_pre).to(dev)[None].contiguous()
+        vv = torch.from_numpy(v).to(dev)[None].contiguous()
+        res = self.batch.decode_step(layer, q, k, vv)
+        host = {name: t[0].cpu().numpy() for name, t in (
+            ("out", res.out), ("hit", res.match_hit), ("use", res.use_hit), ("pos", res.match_pos),
+            ("dist", res.match_dist), ("scan", res.match_scanned), ("flse", res.full_lse),
+            ("rho", res.band_mass), ("cacc", res.cached_acc), ("clse", res.cached_lse), ("fb", res.fallbacks))}
+        self._n[layer] = m
+        ref_rows = None
+        if cfg.oracle_mode:
+            if oracle_rows is not None:
+                ref_rows = np.asarray(oracle_rows, dtype=np.float64)
+            elif host["use"].any():
+                ref_rows = self.batch.attend_full(layer, q)[0].double().cpu().numpy()
+                for h in range(cfg.n_q_heads):
+                    if host["use"][h]:
+                        self.oracle_traffic.record(m, m * self.store.token_bytes)
+
+        delta = DecodeMetrics()
+        outputs = host["out"].astype(np.float64)
+        matches, fulls, cacheds, masses = [], [], [], []
+        errs = [] if cfg.oracle_mode else None
+        for h in range(cfg.n_q_heads):
+            hit = bool(host["hit"][h])
+            mres = MatchResult(hit, int(host["pos"][h]), float(host["dist"][h]), int(host["scan"][h]))
+            delta.match_candidates += mres.candidates_scanned
+            delta.match_bytes += mres.candidates_scanned * self.costs.b_q
+            use = bool(host["use"][h])
+            if hit and not use:
+                delta.forced_misses += 1
+            delta.fallbacks += int(host["fb"][h])
+            if use:
+                tokens = delta.record_hit(m, mres.p, r, self.costs.b_kv)
+                cached = AttentionSummary(host["cacc"][h].astype(np.float64), float(host["clse"][h]),
+                                          max(0, mres.p - r))
+            else:
+                delta.record_miss(m, self.costs.b_kv)
+                tokens = m
+                cached = None
+            self.traffic.record(tokens, tokens * self.store.token_bytes)
+            if errs is not None:
+                ref = outputs[h] if (ref_rows is None or (oracle_rows is None and not use)) else ref_rows[h]
+                num = float(np.linalg.norm(outputs[h] - ref))
+                den = float(np.linalg.norm(ref))
+                err = 0.0 if num == 0.0 else (math.inf if den == 0.0 else num / den)
+                errs.append(err)
+                delta.err_samples.append(err)
+            rho = float(host["rho"][h])
+            matches.append(mres)
+            fulls.append(AttentionSummary(outputs[h], float(host["flse"][h]), m))
+            cacheds.append(cached)
+            masses.append(rho)
+            delta.band_mass_samples.append(rho)
+        for g in range(cfg.n_kv_heads):
+            grp = matches[g * self._group:(g + 1) * self._group]
+            delta.group_kv_tokens += m - min((max(mr.p - r, 0) if mr.hit else 0) for mr in grp)
+            delta.group_kv_total += m
+        self.metrics.merge(delta)
+        return StepResult(outputs=outputs, matches=tuple(matches), full_summaries=tuple(fulls),
+                          cached_summaries=tuple(cacheds), band_masses=tuple(masses),
+                          errs=tuple(errs) if errs is not None else None, delta=delta)
+
+
+def run_decode(trace, cfg: EngineConfig, *, per_step_oracle: bool = False, on_step=None,
+               device="cuda") -> DecodeEngine:
+    """Drive a whole trace through a fresh engine (engine.py:575-607)."""
+    if (trace.d, trace.d_v, trace.n_layers, trace.n_q_heads, trace.n_kv_heads) != (
+            cfg.d, cfg.d_v, cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads):
+        raise ValueError("trace dimensions do not match the engine config")
+    eng = DecodeEngine(cfg, device=device, capacity=int(trace.seq_len))
+    for m in range(1, int(trace.seq_len) + 1):
+        for layer in range(cfg.n_layers):
+            res = eng.decode_step(layer, trace.q_pre[m - 1, layer], trace.k_pre[m - 1, layer],
+                                  trace.v[m - 1, layer], m)
+            if on_step is not None:
+                on_step(m, layer, res)
+    return eng

@@ -1,0 +1,145 @@
+"""CPU-only checks: configuration/metrics parity with the reference, trace I/O,
+and the C-ABI library surface (it loads and exports every declared symbol)."""
+
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2604_00235_b200 import (
+    ByteCostModel,
+    DecodeMetrics,
+    EngineConfig,
+    MatchConfig,
+    MatchResult,
+    SyntheticSpec,
+    TraceError,
+    aux_overhead_ratio,
+    aux_overhead_rule_of_thumb,
+    break_even_gate,
+    compute_metrics,
+    gen_synthetic,
+    group_kv_span,
+    read_trace,
+    threshold,
+    write_trace,
+)
+
+
+def hit_at(p):
+    return MatchResult(hit=True, p=p, sq_dist=0.0, candidates_scanned=1)
+
+
+MISS = MatchResult(hit=False, p=-1, sq_dist=math.inf, candidates_scanned=0)
+
+
+def test_threshold_formula():
+    assert threshold(128, 0.45) ** 2 == pytest.approx(2 * 128 * 0.55 ** 2)
+    assert threshold(2, 0.5) == pytest.approx(1.0)
+    with pytest.raises(ValueError):
+        threshold(4, 1.0)
+
+
+def test_break_even_and_group_span():
+    unit = ByteCostModel(b_kv=1.0, b_q=1.0)
+    assert break_even_gate(1280, 256, 1024, unit) and not break_even_gate(1279, 256, 1024, unit)
+    assert group_kv_span([hit_at(1000), hit_at(1500)], 2000, 256) == 1256
+    assert group_kv_span([hit_at(1000), MISS], 2000, 256) == 2000
+    assert group_kv_span([hit_at(100)], 2000, 256) == 2000
+    with pytest.raises(ValueError):
+        group_kv_span([], 10, 2)
+
+
+def test_aux_overhead():
+    cfg = EngineConfig(d=64, d_v=64, n_q_heads=8, n_kv_heads=8, window=1024)
+    want = 1024 * 8 * (64 + 64 + 2) / (120_000 * 8 * 2 * 64)
+    assert aux_overhead_ratio(cfg, 120_000) == pytest.approx(want, rel=1e-15)
+    assert aux_overhead_rule_of_thumb(1024, 120_000) == pytest.approx(0.05)
+
+
+def test_engine_config_validation():
+    EngineConfig(d=2, d_v=1)
+    EngineConfig(d=128, d_v=128, storage="bf16")
+    for bad in (dict(d=3, d_v=1), dict(d=4, d_v=0), dict(d=4, d_v=4, n_q_heads=3, n_kv_heads=2),
+                dict(d=4, d_v=4, window=0), dict(d=4, d_v=4, band=-1), dict(d=4, d_v=4, tau=1.0),
+                dict(d=4, d_v=4, n_layers=2, tau_per_layer=(0.4,)), dict(d=4, d_v=4, storage="f16"),
+                dict(d=4, d_v=4, downdate_mode="subtract"), dict(d=4, d_v=4, refresh_every=-1)):
+        with pytest.raises(ValueError):
+            EngineConfig(**bad)
+    cfg = EngineConfig(d=4, d_v=4, n_layers=2, tau_per_layer=(0.3, 0.6))
+    assert cfg.tau_for(0) == 0.3 and cfg.tau_for(1) == 0.6
+    with pytest.raises(ValueError):
+        MatchConfig(d=4, tau=1.0)
+
+
+def test_metrics_algebra():
+    m = DecodeMetrics()
+    assert m.record_hit(2000, 1000, 256) == 1256
+    for _ in range(3):
+        m.record_miss(2000)
+    got = compute_metrics(m)
+    assert got["acceptance_rate"] == 0.25
+    assert got["kv_fraction"] == pytest.approx((1256 + 6000) / 8000)
+    assert got["mean_gap"] == 1000.0
+    with pytest.raises(ValueError):
+        compute_metrics(DecodeMetrics())
+
+
+def test_trace_roundtrip_and_errors(tmp_path):
+    tr = gen_synthetic(SyntheticSpec(seq_len=20, d=8, d_v=4, n_layers=2, n_q_heads=4, n_kv_heads=2))
+    write_trace(tr, str(tmp_path / "t"))
+    back = read_trace(str(tmp_path / "t"))
+    for a, b in ((tr.q_pre, back.q_pre), (tr.k_pre, back.k_pre), (tr.v, back.v)):
+        np.testing.assert_array_equal(a, b)
+    with pytest.raises(TraceError):
+        read_trace(str(tmp_path / "missing"))
+    with open(tmp_path / "t" / "v.bin", "wb") as fh:
+        fh.write(b"\0" * 12)
+    with pytest.raises(TraceError):
+        read_trace(str(tmp_path / "t"))
+
+
+def test_synthetic_spec_validation():
+    with pytest.raises(ValueError):
+        SyntheticSpec(seq_len=0)
+    with pytest.raises(ValueError):
+        SyntheticSpec(seq_len=4, d=3)
+    tr = gen_synthetic(SyntheticSpec(seq_len=50, d=16, d_v=8))
+    np.testing.assert_allclose(np.linalg.norm(tr.q_pre.astype(np.float64), axis=-1), 4.0, rtol=1e-6)
+
+
+def _declared_functions():
+    with open(os.path.join(ROOT, "include", "macattn.h")) as fh:
+        src = fh.read()
+    return re.findall(r"^\w[\w\s\*]*?\b(mac_\w+)\s*\(", src, flags=re.M)
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2604_00235_b200 import _lib
+
+    lib = _lib.load()  # raises if missing or ABI/layout mismatched
+    declared = _declared_functions()
+    assert set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    import ctypes
+
+    assert lib.mac_params_size() == ctypes.sizeof(_lib.MacDecodeParams)
+    assert lib.mac_error_string(1002).decode().startswith("macattn")
+
+
+def test_library_rejects_bad_params_without_gpu():
+    """Validation happens before any launch, so it is testable on a CPU box."""
+    from paper_2604_00235_b200 import _lib
+
+    lib = _lib.load()
+    p = _lib.MacDecodeParams()
+    assert lib.mac_decode_step(p, None) == 1002  # zero batch -> shape error
+    p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim, p.head_dim_v = 1, 4, 2, 8, 8
+    p.window, p.band, p.max_chunks, p.min_chunk, p.page_size, p.pages_per_seq = 4, 1, 1, 16, 16, 1
+    assert lib.mac_decode_step(p, None) == 1001  # null pointers
+    p.storage = 7
+    assert lib.mac_decode_step(p, None) == 1003
