@@ -386,6 +386,25 @@ class OracleEngine:
             self.rlse[layer, :, slot] = ring_lse[:, i]
         self.count[layer] = n
 
+    def inject_tail(self, layer, n, k_rows, v_rows, row0, ring_q, ring_acc, ring_lse):
+        """Like inject(), but only K/V rows row0+1..row0+T are given; older rows stay
+        zero (np.zeros pages are mapped lazily, so a 128K-token state costs only its tail)."""
+        self._grow(n + 64)
+        T = k_rows.shape[1]
+        self.K[layer, :, row0 : row0 + T] = k_rows
+        self.V[layer, :, row0 : row0 + T] = v_rows
+        self.n[layer] = n
+        W = self.cfg.window
+        cnt = ring_q.shape[1]
+        pos = np.arange(n - cnt + 1, n + 1)
+        slots = (pos - 1) % W
+        self.rq[layer][:, slots] = ring_q
+        self.rsq[layer][:, slots] = np.einsum("hwd,hwd->hw", ring_q, ring_q)
+        self.rpos[layer][:, slots] = pos
+        self.racc[layer][:, slots] = ring_acc
+        self.rlse[layer][:, slots] = ring_lse
+        self.count[layer] = n
+
     def _live(self, layer, h):
         """Ring view in push order semantics: entries live if pos >= 1 (matching.py:114-117)."""
         n_live = int(min(self.count[layer], self.cfg.window))

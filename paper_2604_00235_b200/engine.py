@@ -152,6 +152,7 @@ class BatchDecodeEngine:
             new_k.append(k)
             new_v.append(v)
         self.k_cache, self.v_cache, self.page_table = new_k, new_v, table
+        self.__dict__.pop("_pcache", None)  # cached launch params hold the old pointers
         self.capacity = pps * ps
 
     def reserve(self, tokens: int):
@@ -161,6 +162,19 @@ class BatchDecodeEngine:
 
     # ------------------------------------------------------------------ launch
     def _params(self, layer: int, q, k, v, in_dt: int, force_miss: bool = False) -> _lib.MacDecodeParams:
+        key = (layer, q.data_ptr(), k.data_ptr(), v.data_ptr(), in_dt, force_miss)
+        cache = self.__dict__.setdefault("_pcache", {})
+        hit = cache.get(key)
+        if hit is not None:
+            return hit
+        P = self._build_params(layer, q, k, v, in_dt, force_miss)
+        if hasattr(self, "workspace"):
+            if len(cache) > 256:
+                cache.clear()
+            cache[key] = P
+        return P
+
+    def _build_params(self, layer: int, q, k, v, in_dt: int, force_miss: bool) -> _lib.MacDecodeParams:
         cfg = self.cfg
         P = _lib.MacDecodeParams()
         P.batch = self.batch
