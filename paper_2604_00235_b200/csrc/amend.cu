@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(128) amend_generic_kernel(MacDecodeParams p, c
       int lo = head_lo(use, use ? p.match_pos[bh] : 0, r);
       if (lo < lo_g) lo_g = lo;
     }
-    const int lo_first = lo_g > p.kv_offset + 1 ? lo_g : p.kv_offset + 1;  // shard-local floor
+    const int lo_first = grid_start(lo_g, p.kv_offset);  // shard-local floor
     const Chunking ch = chunking(m - lo_first + 1, p.max_chunks, p.min_chunk);
     if (c >= ch.n) continue;  // block-uniform
     const int t0 = lo_first + c * ch.len;

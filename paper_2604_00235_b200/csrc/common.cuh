@@ -128,6 +128,17 @@ __host__ __device__ __forceinline__ Chunking chunking(int span, int max_chunks, 
   return c;
 }
 
+// first token of a group's split grid: max(lo_g, first local token) rounded down
+// to a 16-token boundary in shard-local coordinates, so every 16-token sub-tile
+// lies inside one KV page (page_size % 16 == 0).  Tokens below a head's own
+// lo_h are masked by the kernels, so the rounding never changes a result.
+__host__ __device__ __forceinline__ int grid_start(int lo_g, int kv_offset) {
+  int local = lo_g - kv_offset;
+  if (local < 1) local = 1;
+  local = ((local - 1) & ~15) + 1;
+  return local + kv_offset;
+}
+
 // physical row of token t (1-based, local to this KV shard) in a paged cache
 __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table, int pages_per_seq,
                                           int b, int t, int page_size, int n_kv, int kvh) {
@@ -137,14 +148,19 @@ __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table
 }
 
 // workspace layout (bytes, 256-aligned sections)
+// mkey/marr (match keys and arrival counters) must start zeroed: the engine
+// clears the workspace once at allocation and the match kernel re-zeroes them.
 struct Workspace {
-  size_t mpos_off, qrot_off, part_off, total;
+  size_t mkey_off, marr_off, mpos_off, qrot_off, part_off, total;
 };
 __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 __host__ __forceinline__ Workspace workspace_layout(const MacDecodeParams& p) {
   size_t acc = p.storage == MAC_MODE_F64 ? 8 : 4;
   Workspace w;
-  w.mpos_off = 0;
+  const size_t rows = (size_t)p.batch * p.n_q_heads;
+  w.mkey_off = 0;
+  w.marr_off = align256(w.mkey_off + sizeof(unsigned long long) * rows);
+  w.mpos_off = align256(w.marr_off + sizeof(unsigned int) * rows);
   w.qrot_off = align256(w.mpos_off + sizeof(int32_t) * (size_t)p.batch);
   w.part_off = align256(w.qrot_off + acc * (size_t)p.batch * p.n_q_heads * p.head_dim);
   size_t part = acc * (size_t)p.batch * p.n_q_heads * p.max_chunks * 2 * (p.head_dim_v + 1);

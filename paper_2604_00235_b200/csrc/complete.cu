@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const 
     int lo = head_lo(u, u ? p.match_pos[bj] : 0, r);
     if (lo < lo_g) lo_g = lo;
   }
-  const int lo_first = lo_g > p.kv_offset + 1 ? lo_g : p.kv_offset + 1;
+  const int lo_first = grid_start(lo_g, p.kv_offset);
   const Chunking ch = chunking(m - lo_first + 1, p.max_chunks, p.min_chunk);
   const int use = p.force_miss ? 0 : p.use_hit[bh];
   const int pp = use ? p.match_pos[bh] : -1;

@@ -125,7 +125,8 @@ class BatchDecodeEngine:
         self.o_cached_acc = torch.zeros(B, Hq, dv, dtype=self.sumdt, device=dev) if record_cached else None
         self.o_cached_lse = torch.zeros(B, Hq, dtype=self.sumdt, device=dev) if record_cached else None
         probe = self._params(0, self.o_out, self.o_out, self.o_out, _lib.DT_F32)
-        self.workspace = torch.empty(int(_lib.load().mac_workspace_bytes(probe)), dtype=torch.uint8, device=dev)
+        # zeroed once: the match kernel keeps its cross-CTA keys/counters zero between steps
+        self.workspace = torch.zeros(int(_lib.load().mac_workspace_bytes(probe)), dtype=torch.uint8, device=dev)
 
     # ------------------------------------------------------------------ memory
     def _alloc_kv(self, tokens: int):
@@ -290,17 +291,17 @@ class BatchDecodeEngine:
             ids = self.page_table[b, :pages].long()
             kk = torch.zeros(pages * ps, cfg.n_kv_heads, cfg.d, dtype=self.sdt, device=self.device)
             vv = torch.zeros(pages * ps, cfg.n_kv_heads, cfg.d_v, dtype=self.sdt, device=self.device)
-            kk[:n] = k_rot[b].transpose(0, 1).to(self.sdt)
-            vv[:n] = v[b].transpose(0, 1).to(self.sdt)
+            kk[:n] = k_rot[b].transpose(0, 1).to(self.device, self.sdt)
+            vv[:n] = v[b].transpose(0, 1).to(self.device, self.sdt)
             self.k_cache[layer][ids] = kk.view(pages, ps, cfg.n_kv_heads, cfg.d).transpose(1, 2)
             self.v_cache[layer][ids] = vv.view(pages, ps, cfg.n_kv_heads, cfg.d_v).transpose(1, 2)
         cnt = ring_q.shape[2]
         W = cfg.window
         pos = torch.arange(n - cnt + 1, n + 1, device=self.device)
         slots = (pos - 1) % W
-        self.ring_q[layer][:, :, slots] = ring_q.to(self.sdt)
-        self.ring_acc[layer][:, :, slots] = ring_acc.to(self.sumdt)
-        self.ring_lse[layer][:, :, slots] = ring_lse.to(self.sumdt)
+        self.ring_q[layer][:, :, slots] = ring_q.to(self.device, self.sdt)
+        self.ring_acc[layer][:, :, slots] = ring_acc.to(self.device, self.sumdt)
+        self.ring_lse[layer][:, :, slots] = ring_lse.to(self.device, self.sumdt)
         self.seq_lens[layer].fill_(n)
 
 

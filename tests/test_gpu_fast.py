@@ -1,0 +1,141 @@
+"""GPU parity of the bf16 d=128 fast kernels (vectorised match, tensor-core amend).
+
+Checked against the CPU oracle in its bf16 storage mode (equal to the
+reference fed storage-matched keys), on replayed traces and
+on injected long-context state where both hits and misses occur.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import mac_oracle as orc  # noqa: E402
+from golden_util import bf16_round, rel_err  # noqa: E402
+
+TOL = 2e-4
+
+
+def _fast_path_used(eng):
+    from paper_2604_00235_b200 import _lib
+
+    P = eng._params(0, eng.o_out, eng.o_out, eng.o_out, _lib.DT_BF16)
+    return _lib.load().mac_amend_variant(P) == 1
+
+
+@pytest.mark.parametrize("hq,hkv,window,band,delta_max", [
+    (8, 2, 64, 16, None), (16, 2, 100, 0, None), (4, 4, 300, 32, None), (8, 2, 64, 16, 20), (8, 1, 48, 8, None)])
+def test_fast_replay_matches_oracle(hq, hkv, window, band, delta_max):
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    L, B = 400, 2
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=10 + s))
+           for s in range(B)]
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=window, band=band, storage="bf16",
+                       delta_max=delta_max)
+    eng = BatchDecodeEngine(cfg, B, L, page_perm_seed=3, min_chunk=32)
+    assert _fast_path_used(eng)
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=window, band=band,
+                            storage="bf16", delta_max=delta_max)
+    oes = [orc.OracleEngine(ocfg, capacity=L) for _ in range(B)]
+    q = [bf16_round(t.q_pre[:, 0]) for t in trs]
+    k = [bf16_round(t.k_pre[:, 0]) for t in trs]
+    v = [bf16_round(t.v[:, 0]) for t in trs]
+    worst, hits, flips = 0.0, 0, 0
+    for m in range(1, L + 1):
+        qd = torch.from_numpy(np.stack([x[m - 1] for x in q])).to("cuda", torch.bfloat16)
+        kd = torch.from_numpy(np.stack([x[m - 1] for x in k])).to("cuda", torch.bfloat16)
+        vd = torch.from_numpy(np.stack([x[m - 1] for x in v])).to("cuda", torch.bfloat16)
+        res = eng.decode_step(0, qd, kd, vd)
+        gh = res.match_hit.cpu().numpy().astype(bool)
+        gp = res.match_pos.cpu().numpy()
+        go = res.out.double().cpu().numpy()
+        for b in range(B):
+            st = oes[b].decode_step(0, q[b][m - 1], k[b][m - 1], v[b][m - 1], m)
+            flips += int((gh[b] != st.hit).sum() + (gp[b] != st.p).sum())
+            hits += int(st.use_hit.sum())
+            for h in range(hq):
+                worst = max(worst, rel_err(go[b, h], st.outputs[h]))
+    assert flips == 0
+    assert hits > 0
+    assert worst <= TOL, worst
+
+
+def test_fast_long_context_hits_and_misses():
+    """C2-shaped injected state (32K, 32Q/8KV) with 30% fresh queries: misses stream the whole KV."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
+    from paper_2604_00235_b200.synth import request_state
+
+    B, n0, S, hq, hkv, W, r = 2, 32768 - 8, 4, 32, 8, 1024, 256
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, n0 + S + 1)
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    states, oes, kfull, vfull = [], [], [], []
+    for b in range(B):
+        st = request_state(100 + b, n0=n0, steps=S, hq=hq, hkv=hkv, d=128, dv=128, window=W, band=r, rep_prob=0.7)
+        rng = np.random.default_rng(200 + b)
+        kf = bf16_round(rng.standard_normal((hkv, n0, 128))).astype(np.float32)
+        vf = bf16_round(rng.standard_normal((hkv, n0, 128))).astype(np.float32)
+        T = st.tail_k.shape[1]
+        kf[:, n0 - T:] = st.tail_k
+        vf[:, n0 - T:] = st.tail_v
+        states.append(st)
+        kfull.append(kf)
+        vfull.append(vf)
+        oe = orc.OracleEngine(ocfg, capacity=n0 + S + 8)
+        oe.inject(0, kf.astype(np.float64), vf.astype(np.float64), st.ring_q.astype(np.float64),
+                  st.ring_acc.astype(np.float64), st.ring_lse.astype(np.float64))
+        oes.append(oe)
+    eng.inject(0, torch.from_numpy(np.stack(kfull)).cuda(), torch.from_numpy(np.stack(vfull)).cuda(),
+               torch.from_numpy(np.stack([s.ring_q for s in states])).cuda(),
+               torch.from_numpy(np.stack([s.ring_acc for s in states])).cuda(),
+               torch.from_numpy(np.stack([s.ring_lse for s in states])).cuda(), n0)
+    worst, misses, hits = 0.0, 0, 0
+    for s in range(S):
+        qd = torch.from_numpy(np.stack([x.step_q[s] for x in states])).to("cuda", torch.bfloat16)
+        kd = torch.from_numpy(np.stack([x.step_k[s] for x in states])).to("cuda", torch.bfloat16)
+        vd = torch.from_numpy(np.stack([x.step_v[s] for x in states])).to("cuda", torch.bfloat16)
+        res = eng.decode_step(0, qd, kd, vd)
+        go = res.out.double().cpu().numpy()
+        gh = res.match_hit.cpu().numpy().astype(bool)
+        gp = res.match_pos.cpu().numpy()
+        for b in range(B):
+            st = oes[b].decode_step(0, states[b].step_q[s], states[b].step_k[s], states[b].step_v[s], n0 + s + 1)
+            np.testing.assert_array_equal(gh[b], st.hit)
+            np.testing.assert_array_equal(gp[b], st.p)
+            misses += int((~st.use_hit).sum())
+            hits += int(st.use_hit.sum())
+            for h in range(hq):
+                worst = max(worst, rel_err(go[b, h], st.outputs[h]))
+    assert misses > 0 and hits > 0
+    assert worst <= TOL, worst
+
+
+def test_full_decode_long_context_bf16():
+    """Full-attention decode at 32K on the tensor-core path vs exact attention (oracle)."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
+
+    n, hq, hkv = 32768, 16, 2
+    rng = np.random.default_rng(5)
+    k = bf16_round(rng.standard_normal((1, hkv, n, 128)) * 2).astype(np.float32)
+    v = bf16_round(rng.standard_normal((1, hkv, n, 128))).astype(np.float32)
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, storage="bf16")
+    eng = BatchDecodeEngine(cfg, 1, n + 4)
+    W = cfg.window
+    eng.inject(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+               torch.zeros(1, hq, W, 128), torch.zeros(1, hq, W, 128), torch.full((1, hq, W), -math.inf), n)
+    q = bf16_round(rng.standard_normal((hq, 128)))
+    k_new = bf16_round(rng.standard_normal((hkv, 128)))
+    v_new = bf16_round(rng.standard_normal((hkv, 128)))
+    out = eng.full_decode(0, *(torch.from_numpy(a[None]).to("cuda", torch.bfloat16).contiguous()
+                                for a in (q, k_new, v_new))).double().cpu().numpy()[0]
+    freqs = orc.rope_freqs(128)
+    kk = np.concatenate([k[0].astype(np.float64), bf16_round(orc.rope_rotate(k_new, float(n + 1), freqs))[:, None]], 1)
+    vv = np.concatenate([v[0].astype(np.float64), v_new[:, None]], 1)
+    g = hq // hkv
+    for h in range(hq):
+        s = orc.summarize(orc.rope_rotate(q[h], float(n + 1), freqs), kk[h // g], vv[h // g])
+        assert rel_err(out[h], s.acc) <= TOL, h
