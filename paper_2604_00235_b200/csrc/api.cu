@@ -5,14 +5,16 @@
 #include "common.cuh"
 
 namespace mac {
-template <int MODE> cudaError_t launch_append(const MacDecodeParams&, cudaStream_t, int);
+template <int MODE> cudaError_t launch_append(const MacDecodeParams&, cudaStream_t, int, int);
 template <int MODE> cudaError_t launch_match_generic(const MacDecodeParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_amend_generic(const MacDecodeParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_complete(const MacDecodeParams&, cudaStream_t, int);
-cudaError_t launch_match_bf16_d128(const MacDecodeParams&, cudaStream_t);
+cudaError_t launch_front_bf16(const MacDecodeParams&, cudaStream_t, bool do_match, bool do_append, int rotate_only,
+                              int plan);
 cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t);
 bool amend_mma_supported(const MacDecodeParams&);
 bool match_fast_supported(const MacDecodeParams&);
+bool front_fast_supported(const MacDecodeParams&);
 cudaError_t launch_merge_partials(const MacMergeParams&, cudaStream_t);
 }  // namespace mac
 
@@ -38,23 +40,39 @@ static int validate(const MacDecodeParams* p, bool need_ring) {
   return MAC_OK;
 }
 
+enum : int {
+  STAGE_APPEND = 1,         // append K/V at m = seq_lens + 1, rotate q
+  STAGE_MATCH = 2,          // ring match + decision + plan
+  STAGE_AMEND = 4,          // split-KV partials over the plan
+  STAGE_COMPLETE = 8,       // merge, output, ring write-back
+  STAGE_COMPLETE_FULL = 16, // merge and output only (full-attention modes)
+  STAGE_ROTATE = 32,        // rotate q at m = seq_lens, no append
+  STAGE_PLAN_FULL = 64      // plan every group as [1, m] in the append stage
+};
+
 template <int MODE>
-static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int stage_mask) {
+static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int mask) {
   cudaError_t e = cudaSuccess;
-  if (stage_mask & 1) { e = launch_append<MODE>(p, st, 0); if (e) return e; }
-  if (stage_mask & 32) { e = launch_append<MODE>(p, st, 1); if (e) return e; }
-  if (stage_mask & 2) {
-    if (MODE == MAC_MODE_BF16 && match_fast_supported(p)) e = launch_match_bf16_d128(p, st);
-    else e = launch_match_generic<MODE>(p, st);
-    if (e) return e;
+  const bool app = mask & (STAGE_APPEND | STAGE_ROTATE);
+  const int rot = (mask & STAGE_ROTATE) ? 1 : 0, plan = (mask & STAGE_PLAN_FULL) ? 1 : 0;
+  if (MODE == MAC_MODE_BF16 && front_fast_supported(p)) {
+    const bool fast_match = (mask & STAGE_MATCH) && match_fast_supported(p);
+    if (app || fast_match) {
+      e = launch_front_bf16(p, st, fast_match, app, rot, plan);
+      if (e) return e;
+    }
+    if ((mask & STAGE_MATCH) && !fast_match) { e = launch_match_generic<MODE>(p, st); if (e) return e; }
+  } else {
+    if (app) { e = launch_append<MODE>(p, st, rot, plan); if (e) return e; }
+    if (mask & STAGE_MATCH) { e = launch_match_generic<MODE>(p, st); if (e) return e; }
   }
-  if (stage_mask & 4) {
+  if (mask & STAGE_AMEND) {
     if (MODE == MAC_MODE_BF16 && amend_mma_supported(p)) e = launch_amend_mma_bf16(p, st);
     else e = launch_amend_generic<MODE>(p, st);
     if (e) return e;
   }
-  if (stage_mask & 8) { e = launch_complete<MODE>(p, st, 0); if (e) return e; }
-  if (stage_mask & 16) { e = launch_complete<MODE>(p, st, 1); if (e) return e; }
+  if (mask & STAGE_COMPLETE) { e = launch_complete<MODE>(p, st, 0); if (e) return e; }
+  if (mask & STAGE_COMPLETE_FULL) { e = launch_complete<MODE>(p, st, 1); if (e) return e; }
   return e;
 }
 
@@ -94,18 +112,20 @@ int mac_amend_variant(const MacDecodeParams* p) {
   return (p && p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) ? 1 : 0;
 }
 
-int mac_append_kv(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 1, false); }
-int mac_match(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 2, true); }
-int mac_amend(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 4, true); }
-int mac_complete(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 8, true); }
-int mac_decode_step(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, 1 | 2 | 4 | 8, true); }
+int mac_append_kv(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_APPEND, false); }
+int mac_match(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_MATCH, true); }
+int mac_amend(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_AMEND, true); }
+int mac_complete(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_COMPLETE, true); }
+int mac_decode_step(const MacDecodeParams* p, void* stream) {
+  return dispatch(p, stream, STAGE_APPEND | STAGE_MATCH | STAGE_AMEND | STAGE_COMPLETE, true);
+}
 
 int mac_full_decode(const MacDecodeParams* p, void* stream) {
   if (!p) return MAC_ERR_NULL;
   MacDecodeParams q = *p;
   q.force_miss = 1;
   q.band = 0;  // no prefix/band split: one summary over [1, m]
-  return dispatch(&q, stream, 1 | 4 | 16, false);
+  return dispatch(&q, stream, STAGE_APPEND | STAGE_PLAN_FULL | STAGE_AMEND | STAGE_COMPLETE_FULL, false);
 }
 
 int mac_attend_full(const MacDecodeParams* p, void* stream) {
@@ -113,7 +133,7 @@ int mac_attend_full(const MacDecodeParams* p, void* stream) {
   MacDecodeParams q = *p;
   q.force_miss = 1;
   q.band = 0;
-  return dispatch(&q, stream, 32 | 4 | 16, false);
+  return dispatch(&q, stream, STAGE_ROTATE | STAGE_PLAN_FULL | STAGE_AMEND | STAGE_COMPLETE_FULL, false);
 }
 
 int mac_merge_partials(const MacMergeParams* p, void* stream) {

@@ -14,7 +14,7 @@ namespace mac {
 template <int MODE>
 __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int32_t* __restrict__ mpos,
                                                           typename Traits<MODE>::acc_t* __restrict__ qrot,
-                                                          int rotate_only) {
+                                                          int rotate_only, int plan) {
   using kv_t = typename Traits<MODE>::kv_t;
   using acc_t = typename Traits<MODE>::acc_t;
   const int b = blockIdx.x / p.n_kv_heads;
@@ -47,6 +47,11 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
       qrot[qi + 1] = (acc_t)(x0 * s + x1 * c);
     }
   }
+  if (plan && threadIdx.x == 0) {  // full-attention modes: every head reads [1, m]
+    int* lo = ws_ptr<int>(p, workspace_layout(p).lo_off);
+    for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;
+    plan_group(p, b, kvh, m, 1);
+  }
   if (store_kv) {
     for (int e = threadIdx.x; e < dv; e += blockDim.x) {
       int64_t vi = ((int64_t)b * p.n_kv_heads + kvh) * dv + e;
@@ -56,19 +61,19 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
 }
 
 template <int MODE>
-cudaError_t launch_append(const MacDecodeParams& p, cudaStream_t st, int rotate_only) {
+cudaError_t launch_append(const MacDecodeParams& p, cudaStream_t st, int rotate_only, int plan) {
   Workspace w = workspace_layout(p);
   char* ws = static_cast<char*>(p.workspace);
   int threads = p.head_dim / 2;
   threads = threads < 32 ? 32 : (threads > 256 ? 256 : ((threads + 31) / 32) * 32);
   append_rope_kernel<MODE><<<p.batch * p.n_kv_heads, threads, 0, st>>>(
       p, reinterpret_cast<int32_t*>(ws + w.mpos_off),
-      reinterpret_cast<typename Traits<MODE>::acc_t*>(ws + w.qrot_off), rotate_only);
+      reinterpret_cast<typename Traits<MODE>::acc_t*>(ws + w.qrot_off), rotate_only, plan);
   return cudaGetLastError();
 }
 
-template cudaError_t launch_append<MAC_MODE_F32>(const MacDecodeParams&, cudaStream_t, int);
-template cudaError_t launch_append<MAC_MODE_BF16>(const MacDecodeParams&, cudaStream_t, int);
-template cudaError_t launch_append<MAC_MODE_F64>(const MacDecodeParams&, cudaStream_t, int);
+template cudaError_t launch_append<MAC_MODE_F32>(const MacDecodeParams&, cudaStream_t, int, int);
+template cudaError_t launch_append<MAC_MODE_BF16>(const MacDecodeParams&, cudaStream_t, int, int);
+template cudaError_t launch_append<MAC_MODE_F64>(const MacDecodeParams&, cudaStream_t, int, int);
 
 }  // namespace mac

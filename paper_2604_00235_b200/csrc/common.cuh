@@ -148,24 +148,100 @@ __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table
 }
 
 // workspace layout (bytes, 256-aligned sections)
-// mkey/marr (match keys and arrival counters) must start zeroed: the engine
-// clears the workspace once at allocation and the match kernel re-zeroes them.
+// The "persistent" section (match keys, arrival counters, group counters, work
+// list length and work counters) must start zeroed: the engine clears the
+// workspace once at allocation and the kernels return every counter to zero
+// by the end of each step.
 struct Workspace {
-  size_t mkey_off, marr_off, mpos_off, qrot_off, part_off, total;
+  size_t mkey_off;   // [B*Hq] u64   complemented packed (dist, pos) match key
+  size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
+  size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
+  size_t ctr_off;    // [4] u32      work-list length, amend work counter, amend done counter
+  size_t mpos_off;   // [B] i32      position m of this step
+  size_t lo_off;     // [B*Hq] i32   first token each head reads (plan)
+  size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp, c, t0, t1}
+  size_t qrot_off;   // [B*Hq*d]     rotated queries (math dtype)
+  size_t part_off;   // [B*Hq*max_chunks*2*(d_v+1)] split partial summaries
+  size_t total;
 };
 __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-__host__ __forceinline__ Workspace workspace_layout(const MacDecodeParams& p) {
+__host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodeParams& p) {
   size_t acc = p.storage == MAC_MODE_F64 ? 8 : 4;
   Workspace w;
   const size_t rows = (size_t)p.batch * p.n_q_heads;
+  const size_t groups = (size_t)p.batch * p.n_kv_heads;
   w.mkey_off = 0;
-  w.marr_off = align256(w.mkey_off + sizeof(unsigned long long) * rows);
-  w.mpos_off = align256(w.marr_off + sizeof(unsigned int) * rows);
-  w.qrot_off = align256(w.mpos_off + sizeof(int32_t) * (size_t)p.batch);
-  w.part_off = align256(w.qrot_off + acc * (size_t)p.batch * p.n_q_heads * p.head_dim);
-  size_t part = acc * (size_t)p.batch * p.n_q_heads * p.max_chunks * 2 * (p.head_dim_v + 1);
-  w.total = align256(w.part_off + part);
+  w.marr_off = align256(w.mkey_off + 8 * rows);
+  w.gcnt_off = align256(w.marr_off + 4 * rows);
+  w.ctr_off = align256(w.gcnt_off + 4 * groups);
+  w.mpos_off = align256(w.ctr_off + 16);
+  w.lo_off = align256(w.mpos_off + 4 * (size_t)p.batch);
+  w.list_off = align256(w.lo_off + 4 * rows);
+  w.qrot_off = align256(w.list_off + 16 * groups * p.max_chunks);
+  w.part_off = align256(w.qrot_off + acc * rows * p.head_dim);
+  w.total = align256(w.part_off + acc * rows * p.max_chunks * 2 * (p.head_dim_v + 1));
   return w;
+}
+
+template <typename T> __host__ __device__ __forceinline__ T* ws_ptr(const MacDecodeParams& p, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(p.workspace) + off);
+}
+
+// Plan one GQA group: split grid over [grid_start(lo_g), m] and one work item
+// {grp, c, t0, t1} per split appended to the device work list (the paper's
+// load-balancer plan, built on the device with no host synchronisation).
+__device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g) {
+  const int start = grid_start(lo_g, p.kv_offset);
+  const Chunking ch = chunking(m - start + 1, p.max_chunks, p.min_chunk);
+  const Workspace w = workspace_layout(p);
+  unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
+  int4* list = ws_ptr<int4>(p, w.list_off);
+  const unsigned cap = (unsigned)(p.batch * p.n_kv_heads * p.max_chunks);
+  const unsigned base = atomicAdd(ctr, (unsigned)ch.n);
+  const int grp = b * p.n_kv_heads + kvh;
+  for (int c = 0; c < ch.n; ++c) {
+    if (base + c >= cap) break;  // cannot happen when every step is completed
+    const int t0 = start + c * ch.len;
+    const int t1 = min(m, t0 + ch.len - 1);
+    list[base + c] = make_int4(grp, c, t0, t1);
+  }
+}
+
+// Decide one (request, q head) from its best candidate, apply the gates, write
+// the match outputs and the head's first token; the last head of a GQA group
+// to be decided plans the group (matching.py:171-175; engine.py:449-459).
+__device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
+                                            double bdist, int bpos) {
+  const int W = p.window, Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv;
+  const bool hit = n_scan > 0 && have && bdist < p.thr_sq;
+  const int pp = hit ? bpos : -1;
+  bool use = hit;
+  if (use && p.roi_gate && !((double)pp * p.roi_b_kv >= (double)W * p.roi_b_q + (double)p.band * p.roi_b_kv))
+    use = false;
+  if (p.refresh_every > 0 && m % p.refresh_every == 0) use = false;
+  if (p.force_miss) use = false;
+  p.match_hit[bh] = hit;
+  p.match_pos[bh] = pp;
+  p.match_dist[bh] = n_scan > 0 ? bdist : CUDART_INF;
+  p.match_scanned[bh] = n_scan;
+  p.use_hit[bh] = use;
+  const Workspace w = workspace_layout(p);
+  int* lo = ws_ptr<int>(p, w.lo_off);
+  lo[bh] = head_lo(use, pp, p.band);
+  __threadfence();
+  const int b = bh / Hq, h = bh % Hq, kvh = h / g;
+  unsigned int* gcnt = ws_ptr<unsigned int>(p, w.gcnt_off);
+  const unsigned prev = atomicAdd(gcnt + b * Hkv + kvh, 1u);
+  if (prev == (unsigned)g - 1) {
+    gcnt[b * Hkv + kvh] = 0u;
+    __threadfence();
+    int lo_g = m;
+    for (int j = 0; j < g; ++j) {
+      const int l = __ldcg(lo + b * Hq + kvh * g + j);
+      lo_g = l < lo_g ? l : lo_g;
+    }
+    plan_group(p, b, kvh, m, lo_g);
+  }
 }
 
 }  // namespace mac

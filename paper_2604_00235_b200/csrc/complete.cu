@@ -16,17 +16,44 @@
 
 namespace mac {
 
-template <typename A>
-__device__ __forceinline__ double merged_lse(const A* base, int n, int stride) {
-  double mx = -CUDART_INF;
-  for (int c = 0; c < n; ++c) mx = fmax(mx, (double)base[(int64_t)c * stride]);
-  if (mx == -CUDART_INF) return mx;
-  double s = 0.0;
-  for (int c = 0; c < n; ++c) {
-    double l = (double)base[(int64_t)c * stride];
-    if (l != -CUDART_INF) s += exp(l - mx);
+// block-wide max / sum over 128 threads
+__device__ __forceinline__ double block_reduce(double v, bool is_max, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, x) : v + x;
   }
-  return mx + log(s);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = is_max ? fmax(v, red[w]) : v + red[w];
+  return v;
+}
+
+// merge n split partials of one set: lse into L, per-split weights exp(l_c - L) into wts
+template <typename A>
+__device__ __forceinline__ double merge_weights(const A* base, int n, int stride, double* wts, double* red) {
+  double mx = -CUDART_INF;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) mx = fmax(mx, (double)base[(int64_t)c * stride]);
+  mx = block_reduce(mx, true, red);
+  if (mx == -CUDART_INF) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) wts[c] = 0.0;
+    return mx;
+  }
+  double sum = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const double l = (double)base[(int64_t)c * stride];
+    sum += l == -CUDART_INF ? 0.0 : exp(l - mx);
+  }
+  sum = block_reduce(sum, false, red);
+  const double L = mx + log(sum);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const double l = (double)base[(int64_t)c * stride];
+    wts[c] = l == -CUDART_INF ? 0.0 : exp(l - L);
+  }
+  return L;
 }
 
 template <int MODE>
@@ -36,32 +63,36 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const 
   using kv_t = typename Traits<MODE>::kv_t;
   using A = typename Traits<MODE>::acc_t;
   using S = typename Traits<MODE>::sum_t;
+  extern __shared__ double wsm[];  // [2][max_chunks] split weights
+  __shared__ double red[32];
   const int bh = blockIdx.x;
   const int b = bh / p.n_q_heads, h = bh % p.n_q_heads;
   const int Hkv = p.n_kv_heads, g = p.n_q_heads / Hkv, kvh = h / g, hl = h % g;
   const int d = p.head_dim, dv = p.head_dim_v, W = p.window, r = p.band, dvp = dv + 1;
   const int m = mpos[b];
+  const int* plan_lo = ws_ptr<const int>(p, workspace_layout(p).lo_off);
 
   int lo_g = m;
   for (int j = 0; j < g; ++j) {
-    int bj = b * p.n_q_heads + kvh * g + j;
-    int u = p.force_miss ? 0 : p.use_hit[bj];
-    int lo = head_lo(u, u ? p.match_pos[bj] : 0, r);
-    if (lo < lo_g) lo_g = lo;
+    const int l = plan_lo[b * p.n_q_heads + kvh * g + j];
+    lo_g = l < lo_g ? l : lo_g;
   }
   const int lo_first = grid_start(lo_g, p.kv_offset);
   const Chunking ch = chunking(m - lo_first + 1, p.max_chunks, p.min_chunk);
   const int use = p.force_miss ? 0 : p.use_hit[bh];
   const int pp = use ? p.match_pos[bh] : -1;
-  const int lo = head_lo(use, pp, r);
+  const int lo = plan_lo[bh];
   const int cpos = m - r;
 
   // partial slots of this head: (grp, c, hl, set) -> stride between splits
   const int grp = b * Hkv + kvh;
   const A* pbase = part + ((int64_t)grp * p.max_chunks * g + hl) * 2 * dvp;
   const int cstride = g * 2 * dvp;
-  const double Lp = merged_lse(pbase + dv, ch.n, cstride);          // piece
-  const double Lb = merged_lse(pbase + dvp + dv, ch.n, cstride);    // band
+  double* wp_s = wsm;
+  double* wb_s = wsm + p.max_chunks;
+  const double Lp = merge_weights(pbase + dv, ch.n, cstride, wp_s, red);         // piece
+  const double Lb = merge_weights(pbase + dvp + dv, ch.n, cstride, wb_s, red);   // band
+  __syncthreads();
 
   // cached summary at p (covers [1, max(0, p-r)]); empty on a miss
   const S* racc = static_cast<const S*>(p.ring_acc);
@@ -110,16 +141,12 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const 
   const int64_t wslot = (int64_t)bh * W + (m - 1) % W;
   for (int e = threadIdx.x; e < dv; e += blockDim.x) {
     double pacc = 0.0, bacc = 0.0;
-    if (Lp != -CUDART_INF)
-      for (int c = 0; c < ch.n; ++c) {
-        double l = (double)pbase[(int64_t)c * cstride + dv];
-        if (l != -CUDART_INF) pacc += (double)pbase[(int64_t)c * cstride + e] * exp(l - Lp);
-      }
-    if (Lb != -CUDART_INF)
-      for (int c = 0; c < ch.n; ++c) {
-        double l = (double)pbase[(int64_t)c * cstride + dvp + dv];
-        if (l != -CUDART_INF) bacc += (double)pbase[(int64_t)c * cstride + dvp + e] * exp(l - Lb);
-      }
+    for (int c = 0; c < ch.n; ++c) {
+      const A* pc = pbase + (int64_t)c * cstride;
+      const double fp = wp_s[c], fb = wb_s[c];
+      if (fp != 0.0) pacc += (double)pc[e] * fp;
+      if (fb != 0.0) bacc += (double)pc[dvp + e] * fb;
+    }
     double aacc = use ? (double)racc[cslot * dv + e] : 0.0;
     // merge keeps an empty side's partner bit-exact (weight exp(0) == 1)
     double pre = (La == -CUDART_INF) ? pacc : (Lp == -CUDART_INF ? aacc : aacc * wa + pacc * wp);
@@ -147,6 +174,7 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const 
       if (p.fallbacks) p.fallbacks[bh] = fell_back;
     }
     if (h == 0) p.seq_lens[b] = m;
+    if (bh == 0) ws_ptr<unsigned int>(p, workspace_layout(p).ctr_off)[0] = 0u;  // work list consumed
   }
 }
 
@@ -154,7 +182,7 @@ template <int MODE>
 cudaError_t launch_complete(const MacDecodeParams& p, cudaStream_t st, int full_mode) {
   Workspace w = workspace_layout(p);
   char* ws = static_cast<char*>(p.workspace);
-  complete_kernel<MODE><<<p.batch * p.n_q_heads, 128, 0, st>>>(
+  complete_kernel<MODE><<<p.batch * p.n_q_heads, 128, 2 * sizeof(double) * p.max_chunks, st>>>(
       p, reinterpret_cast<const int32_t*>(ws + w.mpos_off),
       reinterpret_cast<const typename Traits<MODE>::acc_t*>(ws + w.part_off), full_mode);
   return cudaGetLastError();

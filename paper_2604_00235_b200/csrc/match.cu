@@ -75,18 +75,7 @@ __global__ void __launch_bounds__(256) match_generic_kernel(MacDecodeParams p, c
   if (threadIdx.x == 0) {
     for (int w = 1; w < nwarps; ++w)
       if (better(wbest[w], wpos[w], best, bpos)) { best = wbest[w]; bpos = wpos[w]; }
-    const bool hit = n_scan > 0 && (double)best < p.thr_sq;
-    const int pp = hit ? bpos : -1;
-    bool use = hit;
-    if (use && p.roi_gate && !((double)pp * p.roi_b_kv >= (double)W * p.roi_b_q + (double)p.band * p.roi_b_kv))
-      use = false;
-    if (p.refresh_every > 0 && m % p.refresh_every == 0) use = false;
-    if (p.force_miss) use = false;
-    p.match_hit[bh] = hit;
-    p.match_pos[bh] = pp;
-    p.match_dist[bh] = n_scan > 0 ? (double)best : CUDART_INF;
-    p.match_scanned[bh] = n_scan;
-    p.use_hit[bh] = use;
+    decide_head(p, bh, m, n_scan, bpos > 0, (double)best, bpos);
   }
 }
 

@@ -54,9 +54,10 @@ def rope_freqs(d: int, base: float) -> np.ndarray:
 
 
 def default_max_chunks(batch: int, n_kv_heads: int) -> int:
-    """Split-KV slots per (request, kv head): enough items for ~8 per SM when every head misses."""
+    """Split-KV slots per (request, kv head): when every head misses, about four work items
+    per resident amend warp (8 per SM), so the dynamic scheduler balances the tail."""
     groups = batch * n_kv_heads
-    return int(min(1024, max(8, math.ceil(SM_COUNT_B200 * 8 / groups))))
+    return int(min(2048, max(8, math.ceil(SM_COUNT_B200 * 8 * 4 / groups))))
 
 
 @dataclass
@@ -80,7 +81,7 @@ class BatchDecodeEngine:
     """Batched MAC decode state on one GPU; B independent requests, n_layers layers."""
 
     def __init__(self, cfg: EngineConfig, batch: int, max_seq_len: int, *, device="cuda",
-                 max_chunks: int | None = None, min_chunk: int = 256, page_perm_seed: int | None = None,
+                 max_chunks: int | None = None, min_chunk: int = 128, page_perm_seed: int | None = None,
                  record_cached: bool = False, kv_offset: int = 0):
         if batch < 1:
             raise ValueError("batch must be >= 1")
