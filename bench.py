@@ -272,7 +272,7 @@ def run_ours(args, wl):
     W_, K = args.warmup, args.steps
     cfg = EngineConfig(d=D, d_v=D, n_q_heads=hq, n_kv_heads=hkv, window=WINDOW, band=BAND, tau=TAU, storage="bf16",
                        page_size=args.page_size)
-    eng = BatchDecodeEngine(cfg, B, wl["ctx"] + args.full_steps + 64, device=dev)
+    eng = BatchDecodeEngine(cfg, B, wl["ctx"] + args.full_steps + 64, device=dev, min_chunk=args.min_chunk)
     inject_into_engine(eng, 0, states, n0, bulk_seed=rank)
     bf = torch.bfloat16
     q_all = torch.from_numpy(np.stack([s.step_q for s in states], 1)).to(dev, bf)  # [S, B, Hq, d]
@@ -298,6 +298,7 @@ def run_ours(args, wl):
     with ClockSampler(local) as clk:
         for s in range(S):
             flush.zero_()
+            torch.cuda._sleep(200_000)  # keep the host ahead of the device: no launch gaps inside the step
             sev[s][0].record(stream)
             eng.decode_step(0, q_all[s], k_all[s], v_all[s])
             sev[s][1].record(stream)
@@ -311,6 +312,7 @@ def run_ours(args, wl):
         torch.cuda.synchronize(dev)
         for s in range(S):
             flush.zero_()
+            torch.cuda._sleep(400_000)  # ~0.2 ms of GPU spin: the stage launches queue up behind it
             q, k, v = q_all[s], k_all[s], v_all[s]
             ev[s][0].record(stream)
             for i, name in enumerate(stages):
@@ -456,6 +458,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--page-size", type=int, default=16)
+    ap.add_argument("--min-chunk", type=int, default=128)
     ap.add_argument("--full-steps", type=int, default=10)
     ap.add_argument("--cpu-procs", type=int, default=8)
     ap.add_argument("--cpu-steps", type=int, default=12)

@@ -24,14 +24,14 @@
 // cp.async into an XOR-swizzled 3-stage ring (conflict-free ldmatrix).  The
 // piece -> band switch happens in-stream: the piece partial is written out
 // and the online-softmax state reset without draining the pipeline.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mac {
 
 namespace {
-constexpr int ST = 3;                 // cp.async stages
 constexpr int TILE_BYTES = 16 * 256;  // 16 tokens x 128 dims x bf16
-constexpr int SMEM = ST * 2 * TILE_BYTES;  // 24 KiB per warp
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
@@ -133,8 +133,8 @@ __device__ __forceinline__ void write_partial(const State& S, float* out, int se
   const float inv = Z > 0.f ? 1.f / Z : 0.f;
 #pragma unroll
   for (int nt = 0; nt < 16; ++nt) {
-    *reinterpret_cast<float2*>(o + nt * 8 + q4 * 2) =
-        make_float2((S.o[nt][0] + S.o[nt][2]) * inv, (S.o[nt][1] + S.o[nt][3]) * inv);
+    o[nt * 8 + q4 * 2] = (S.o[nt][0] + S.o[nt][2]) * inv;  // rows of 129 floats: scalar stores
+    o[nt * 8 + q4 * 2 + 1] = (S.o[nt][1] + S.o[nt][3]) * inv;
   }
   if (q4 == 0) o[128] = Z > 0.f ? S.M * LN2 + logf(Z) : -CUDART_INF_F;
 }
@@ -146,7 +146,8 @@ bool amend_mma_supported(const MacDecodeParams& p) {
          p.page_size % 16 == 0;
 }
 
-__global__ void __launch_bounds__(32, 8) amend_mma_kernel(MacDecodeParams p) {
+template <int ST, int MINB>  // cp.async stages per warp, min resident warps per SM (register budget)
+__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x;
   const int Hkv = p.n_kv_heads, Hq = p.n_q_heads, g = Hq / Hkv, r = p.band, ps = p.page_size;
@@ -164,14 +165,56 @@ __global__ void __launch_bounds__(32, 8) amend_mma_kernel(MacDecodeParams p) {
   const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(p.v_cache);
   const unsigned n_items = __ldcg(ctr);
 
+  // the next item's index and plan entry are fetched one item ahead, so the
+  // atomic and the list load are off the critical path after the first item
+  unsigned next = 0;
+  if (lane == 0) next = atomicAdd(ctr + 1, 1u);
+  next = __shfl_sync(0xffffffffu, next, 0);
+  int4 next_it = next < n_items ? list[next] : make_int4(0, 0, 0, 0);
   for (;;) {
-    unsigned item = 0;
-    if (lane == 0) item = atomicAdd(ctr + 1, 1u);
-    item = __shfl_sync(0xffffffffu, item, 0);
+    const unsigned item = next;
     if (item >= n_items) break;
-    const int4 it = list[item];
+    const int4 it = next_it;
+    if (lane == 0) next = atomicAdd(ctr + 1, 1u);
+    next = __shfl_sync(0xffffffffu, next, 0);
     const int grp = it.x, c = it.y, t0 = it.z, t1 = it.w;
     const int b = grp / Hkv, kvh = grp % Hkv;
+    const int nsub = ((t1 - t0) >> 4) + 1;
+    // page rows of the item's sub-tiles, 32 at a time (lane j holds sub-tile 32*blk + j),
+    // fetched one block ahead so the cp.async issue never waits on the page table
+    auto rows_of = [&](int blk) -> long long {
+      const int j = blk * 32 + lane;
+      if (j >= nsub) return 0;
+      const int local = t0 + (j << 4) - p.kv_offset;
+      const int page = p.page_table[(int64_t)b * p.pages_per_seq + (local - 1) / ps];
+      return ((long long)page * Hkv + kvh) * ps + ((local - 1) % ps);
+    };
+    long long rows_cur = rows_of(0), rows_nxt = nsub > 32 ? rows_of(1) : 0;
+    int blk_cur = 0;
+    auto issue = [&](int j, int stage) {
+      if ((j >> 5) != blk_cur) {
+        blk_cur = j >> 5;
+        rows_cur = rows_nxt;
+        rows_nxt = rows_of(blk_cur + 1);
+      }
+      const long long row0 = __shfl_sync(0xffffffffu, rows_cur, j & 31);
+      const char* kg = reinterpret_cast<const char*>(kc + row0 * 128);
+      const char* vg = reinterpret_cast<const char*>(vc + row0 * 128);
+      const uint32_t ks_ = sm + stage * 2 * TILE_BYTES, vs_ = ks_ + TILE_BYTES;
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        const int ci = lane + 32 * rr, trow = ci >> 4, col = ci & 15;
+        cp_async16(ks_ + swz(trow, col), kg + trow * 256 + col * 16);
+        cp_async16(vs_ + swz(trow, col), vg + trow * 256 + col * 16);
+      }
+    };
+    // KV streams first; the query fragments and head bounds load underneath
+#pragma unroll
+    for (int i = 0; i < ST; ++i) {
+      if (i < nsub) issue(i, i);
+      cp_commit();
+    }
+    if (next < n_items) next_it = list[next];
     const int m = mpos[b];
     const int cpos = m - r;
     const int lo_h = row < g ? plan_lo[b * Hq + kvh * g + row] : (1 << 30);
@@ -197,26 +240,6 @@ __global__ void __launch_bounds__(32, 8) amend_mma_kernel(MacDecodeParams p) {
       }
     }
     float* out = part + ((int64_t)(grp * p.max_chunks + c) * g) * 2 * 129;
-    const int nsub = ((t1 - t0) >> 4) + 1;
-    auto issue = [&](int j, int stage) {
-      const int local = t0 + (j << 4) - p.kv_offset;
-      const int page = p.page_table[(int64_t)b * p.pages_per_seq + (local - 1) / ps];
-      const int64_t row0 = ((int64_t)page * Hkv + kvh) * ps + ((local - 1) % ps);
-      const char* kg = reinterpret_cast<const char*>(kc + row0 * 128);
-      const char* vg = reinterpret_cast<const char*>(vc + row0 * 128);
-      const uint32_t ks_ = sm + stage * 2 * TILE_BYTES, vs_ = ks_ + TILE_BYTES;
-#pragma unroll
-      for (int rr = 0; rr < 8; ++rr) {
-        const int ci = lane + 32 * rr, trow = ci >> 4, col = ci & 15;
-        cp_async16(ks_ + swz(trow, col), kg + trow * 256 + col * 16);
-        cp_async16(vs_ + swz(trow, col), vg + trow * 256 + col * 16);
-      }
-    };
-#pragma unroll
-    for (int i = 0; i < ST; ++i) {
-      if (i < nsub) issue(i, i);
-      cp_commit();
-    }
     State S;
     S.reset();
     bool in_band = false;
@@ -274,21 +297,36 @@ __global__ void __launch_bounds__(32, 8) amend_mma_kernel(MacDecodeParams p) {
   }
 }
 
+// Variants (stages, min warps per SM); MAC_AMEND_VARIANT selects one (development knob).
+struct AmendVariant {
+  void (*fn)(MacDecodeParams);
+  int smem;
+};
+static const AmendVariant kAmendVariants[] = {
+    {amend_mma_kernel<3, 8>, 3 * 2 * TILE_BYTES},  {amend_mma_kernel<2, 12>, 2 * 2 * TILE_BYTES},
+    {amend_mma_kernel<2, 10>, 2 * 2 * TILE_BYTES}, {amend_mma_kernel<3, 9>, 3 * 2 * TILE_BYTES},
+    {amend_mma_kernel<4, 7>, 4 * 2 * TILE_BYTES},  {amend_mma_kernel<2, 14>, 2 * 2 * TILE_BYTES},
+};
+
 cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st) {
-  static int blocks_per_sm = 0, sms = 0;
-  if (!blocks_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(amend_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  static int grid_full = 0, vi = 0;
+  if (!grid_full) {
+    const char* env = getenv("MAC_AMEND_VARIANT");
+    vi = env ? atoi(env) : 0;
+    if (vi < 0 || vi >= (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0]))) vi = 0;
+    const AmendVariant& v = kAmendVariants[vi];
+    cudaError_t e = cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
     if (e != cudaSuccess) return e;
-    int dev = 0;
+    int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, amend_mma_kernel, 32, SMEM);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, 32, v.smem);
+    grid_full = sms * (per_sm < 1 ? 1 : per_sm);
   }
+  const AmendVariant& v = kAmendVariants[vi];
   const long cap = (long)p.batch * p.n_kv_heads * p.max_chunks;
-  long grid = (long)sms * blocks_per_sm;
-  if (grid > cap) grid = cap;
-  amend_mma_kernel<<<(int)grid, 32, SMEM, st>>>(p);
+  const int grid = (int)(grid_full < cap ? grid_full : cap);
+  v.fn<<<grid, 32, v.smem, st>>>(p);
   return cudaGetLastError();
 }
 

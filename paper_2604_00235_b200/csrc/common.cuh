@@ -19,18 +19,21 @@ template <> struct Traits<MAC_MODE_F32> {
   using sum_t = float;   // engine.py:397-399 prefix.astype(f32)
   using acc_t = float;   // in-kernel accumulation
   using dist_t = double; // match distances (reference: f64)
+  using merge_t = double;  // summary merge algebra (reference: f64)
 };
 template <> struct Traits<MAC_MODE_BF16> {
   using kv_t = __nv_bfloat16;
   using sum_t = float;
   using acc_t = float;
   using dist_t = float;
+  using merge_t = float;  // serving storage: fp32 merges (well inside the bf16 budget)
 };
 template <> struct Traits<MAC_MODE_F64> {
   using kv_t = double;
   using sum_t = double;
   using acc_t = double;
   using dist_t = double;
+  using merge_t = double;
 };
 
 // ---------------------------------------------------------------------------
@@ -87,6 +90,14 @@ __device__ __forceinline__ double logaddexp(double a, double b) {
   double mx = a > b ? a : b, mn = a > b ? b : a;
   return mx + log1p(exp(mn - mx));
 }
+__device__ __forceinline__ float logaddexp(float a, float b) {
+  if (a == -CUDART_INF_F) return b;
+  if (b == -CUDART_INF_F) return a;
+  const float mx = a > b ? a : b, mn = a > b ? b : a;
+  return mx + log1pf(__expf(mn - mx));
+}
+__device__ __forceinline__ float fexpm1(float x) { return expm1f(x); }
+__device__ __forceinline__ double fexpm1(double x) { return expm1(x); }
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

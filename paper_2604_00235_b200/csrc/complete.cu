@@ -16,46 +16,13 @@
 
 namespace mac {
 
-// block-wide max / sum over 128 threads
-__device__ __forceinline__ double block_reduce(double v, bool is_max, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double x = __shfl_xor_sync(0xffffffffu, v, o);
-    v = is_max ? fmax(v, x) : v + x;
-  }
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  v = red[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = is_max ? fmax(v, red[w]) : v + red[w];
-  return v;
-}
+constexpr int kElems = 4;   // d_v elements per lane per pass (d_v <= 128 in one pass)
+constexpr int kSplits = 8;  // splits whose partials are loaded in one batch
 
-// merge n split partials of one set: lse into L, per-split weights exp(l_c - L) into wts
-template <typename A>
-__device__ __forceinline__ double merge_weights(const A* base, int n, int stride, double* wts, double* red) {
-  double mx = -CUDART_INF;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) mx = fmax(mx, (double)base[(int64_t)c * stride]);
-  mx = block_reduce(mx, true, red);
-  if (mx == -CUDART_INF) {
-    for (int c = threadIdx.x; c < n; c += blockDim.x) wts[c] = 0.0;
-    return mx;
-  }
-  double sum = 0.0;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const double l = (double)base[(int64_t)c * stride];
-    sum += l == -CUDART_INF ? 0.0 : exp(l - mx);
-  }
-  sum = block_reduce(sum, false, red);
-  const double L = mx + log(sum);
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const double l = (double)base[(int64_t)c * stride];
-    wts[c] = l == -CUDART_INF ? 0.0 : exp(l - L);
-  }
-  return L;
-}
-
+// One warp per (request, q head), 4 heads per CTA.  The merge is latency-bound,
+// so memory is touched in two hops: (A) the step's scalars, (B) every partial,
+// the cached ring summary and the query row, all issued before any use; the
+// algebra then runs from registers.
 template <int MODE>
 __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const int32_t* __restrict__ mpos,
                                                        const typename Traits<MODE>::acc_t* __restrict__ part,
@@ -63,74 +30,111 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const 
   using kv_t = typename Traits<MODE>::kv_t;
   using A = typename Traits<MODE>::acc_t;
   using S = typename Traits<MODE>::sum_t;
-  extern __shared__ double wsm[];  // [2][max_chunks] split weights
-  __shared__ double red[32];
-  const int bh = blockIdx.x;
+  using D = typename Traits<MODE>::merge_t;  // merge algebra: fp32 for bf16 storage, fp64 otherwise
+  using M = A;
+  const int lane = threadIdx.x & 31;
+  const int bh = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (bh >= p.batch * p.n_q_heads) return;
   const int b = bh / p.n_q_heads, h = bh % p.n_q_heads;
   const int Hkv = p.n_kv_heads, g = p.n_q_heads / Hkv, kvh = h / g, hl = h % g;
   const int d = p.head_dim, dv = p.head_dim_v, W = p.window, r = p.band, dvp = dv + 1;
-  const int m = mpos[b];
   const int* plan_lo = ws_ptr<const int>(p, workspace_layout(p).lo_off);
+  const D NINF = neg_inf<D>();
 
-  int lo_g = m;
-  for (int j = 0; j < g; ++j) {
-    const int l = plan_lo[b * p.n_q_heads + kvh * g + j];
-    lo_g = l < lo_g ? l : lo_g;
-  }
-  const int lo_first = grid_start(lo_g, p.kv_offset);
-  const Chunking ch = chunking(m - lo_first + 1, p.max_chunks, p.min_chunk);
+  // ---- hop A: scalars of this step ----
+  const int m = mpos[b];
   const int use = p.force_miss ? 0 : p.use_hit[bh];
-  const int pp = use ? p.match_pos[bh] : -1;
+  const int pp_raw = p.force_miss ? -1 : p.match_pos[bh];
   const int lo = plan_lo[bh];
+  int lo_g = 1 << 30;
+  for (int j = lane; j < g; j += 32) lo_g = min(lo_g, plan_lo[b * p.n_q_heads + kvh * g + j]);
+  double qv[kElems];  // exact input values  // this lane's slice of the pre-RoPE query (ring write-back)
+  if (!full_mode) {
+#pragma unroll
+    for (int k = 0; k < kElems; ++k) {
+      const int e = lane + 32 * k;
+      qv[k] = e < d ? load_in(p.q_pre, (int64_t)bh * d + e, p.in_dtype) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, o));
+  lo_g = min(lo_g, m);
+  const int pp = use ? pp_raw : -1;
+  const Chunking ch = chunking(m - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks, p.min_chunk);
   const int cpos = m - r;
-
-  // partial slots of this head: (grp, c, hl, set) -> stride between splits
   const int grp = b * Hkv + kvh;
   const A* pbase = part + ((int64_t)grp * p.max_chunks * g + hl) * 2 * dvp;
   const int cstride = g * 2 * dvp;
-  double* wp_s = wsm;
-  double* wb_s = wsm + p.max_chunks;
-  const double Lp = merge_weights(pbase + dv, ch.n, cstride, wp_s, red);         // piece
-  const double Lb = merge_weights(pbase + dvp + dv, ch.n, cstride, wb_s, red);   // band
-  __syncthreads();
-
-  // cached summary at p (covers [1, max(0, p-r)]); empty on a miss
   const S* racc = static_cast<const S*>(p.ring_acc);
   const S* rlse = static_cast<const S*>(p.ring_lse);
-  double La = -CUDART_INF;
-  int64_t cslot = 0;
-  if (use) {
-    cslot = (int64_t)bh * W + (pp - 1) % W;
-    La = (double)rlse[cslot];
+  const int64_t cslot = use ? (int64_t)bh * W + (pp - 1) % W : 0;
+
+  // ---- hop B: cached summary + split lse values ----
+  const D La = use ? (D)rlse[cslot] : NINF;
+  A lse_p[kSplits], lse_b[kSplits];
+#pragma unroll
+  for (int i = 0; i < kSplits; ++i) {
+    const bool ok = i < ch.n;
+    lse_p[i] = ok ? __ldg(pbase + (int64_t)i * cstride + dv) : neg_inf<A>();
+    lse_b[i] = ok ? __ldg(pbase + (int64_t)i * cstride + dvp + dv) : neg_inf<A>();
   }
+  // log-sum-exp over all splits (splits beyond kSplits: strided loop, rare)
+  D mp = NINF, mb = NINF;
+#pragma unroll
+  for (int i = 0; i < kSplits; ++i) { mp = fmax(mp, (D)lse_p[i]); mb = fmax(mb, (D)lse_b[i]); }
+  for (int c = kSplits + lane; c < ch.n; c += 32) {
+    mp = fmax(mp, (D)__ldg(pbase + (int64_t)c * cstride + dv));
+    mb = fmax(mb, (D)__ldg(pbase + (int64_t)c * cstride + dvp + dv));
+  }
+  if (ch.n > kSplits) { mp = warp_max(mp); mb = warp_max(mb); }
+  D sp = 0.0, sb = 0.0;
+#pragma unroll
+  for (int i = 0; i < kSplits; ++i) {
+    if (mp != NINF && (D)lse_p[i] != NINF) sp += fexp((D)lse_p[i] - mp);
+    if (mb != NINF && (D)lse_b[i] != NINF) sb += fexp((D)lse_b[i] - mb);
+  }
+  if (ch.n > kSplits) {
+    D sp2 = 0.0, sb2 = 0.0;
+    for (int c = kSplits + lane; c < ch.n; c += 32) {
+      const D l1 = (D)__ldg(pbase + (int64_t)c * cstride + dv);
+      const D l2 = (D)__ldg(pbase + (int64_t)c * cstride + dvp + dv);
+      if (l1 != NINF) sp2 += fexp(l1 - mp);
+      if (l2 != NINF) sb2 += fexp(l2 - mb);
+    }
+    sp += warp_sum(sp2);
+    sb += warp_sum(sb2);
+  }
+  const D Lp = mp == NINF ? NINF : mp + flog(sp);  // piece
+  const D Lb = mb == NINF ? NINF : mb + flog(sb);  // band
+
   // prefix = cached (+) piece, full = prefix (+) band (attention.py:119-135)
-  const double Lpre = logaddexp(La, Lp);
-  const double Lfull = logaddexp(Lpre, Lb);
-  const double wa = La == -CUDART_INF ? 0.0 : exp(La - Lpre);
-  const double wp = Lp == -CUDART_INF ? 0.0 : exp(Lp - Lpre);
-  const double wpre = Lpre == -CUDART_INF ? 0.0 : exp(Lpre - Lfull);
-  const double wb = Lb == -CUDART_INF ? 0.0 : exp(Lb - Lfull);
+  const D Lpre = logaddexp(La, Lp);
+  const D Lfull = logaddexp(Lpre, Lb);
+  const D wa = La == NINF ? (D)0 : fexp(La - Lpre);
+  const D wp = Lp == NINF ? (D)0 : fexp(Lp - Lpre);
+  const D wpre = Lpre == NINF ? (D)0 : fexp(Lpre - Lfull);
+  const D wb = Lb == NINF ? (D)0 : fexp(Lb - Lfull);
 
   // token counts (for remove() and rho): band = [max(lo, cpos+1), m]
-  int bstart = lo > cpos + 1 ? lo : cpos + 1;
+  const int bstart = lo > cpos + 1 ? lo : cpos + 1;
   const int bcount = m - bstart + 1 > 0 ? m - bstart + 1 : 0;
   const int pcount = m - bcount;
 
   // optional downdate prefix = remove(full, band) (engine.py:474-478, 494-498)
   int do_remove = 0, fell_back = 0;
-  double Lrem = -CUDART_INF, wr_full = 0.0, wr_band = 0.0;
+  D Lrem = NINF, wr_full = 0, wr_band = 0;
   if (!full_mode && p.downdate == MAC_DOWNDATE_REMOVE && bcount > 0 && (use || pcount > 0)) {
     if (bcount == m) {
-      if (Lb == Lfull) { do_remove = 1; Lrem = -CUDART_INF; }  // whole == band: empty prefix
+      if (Lb == Lfull) { do_remove = 1; Lrem = NINF; }  // whole == band: empty prefix
       else fell_back = 1;
     } else {
-      double diff = Lfull - Lb;
+      const D diff = Lfull - Lb;
       if (diff < p.eps_cancel) fell_back = 1;  // CancellationError (or mass exceeded) -> keep split
       else {
         do_remove = 1;
-        Lrem = Lb + log(expm1(diff));
-        wr_full = exp(Lfull - Lrem);
-        wr_band = exp(Lb - Lrem);
+        Lrem = Lb + flog(fexpm1(diff));
+        wr_full = fexp(Lfull - Lrem);
+        wr_band = fexp(Lb - Lrem);
       }
     }
   }
@@ -139,37 +143,76 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, const 
   kv_t* rq = static_cast<kv_t*>(p.ring_q);
   S* racc_w = static_cast<S*>(p.ring_acc);
   const int64_t wslot = (int64_t)bh * W + (m - 1) % W;
-  for (int e = threadIdx.x; e < dv; e += blockDim.x) {
-    double pacc = 0.0, bacc = 0.0;
-    for (int c = 0; c < ch.n; ++c) {
-      const A* pc = pbase + (int64_t)c * cstride;
-      const double fp = wp_s[c], fb = wb_s[c];
-      if (fp != 0.0) pacc += (double)pc[e] * fp;
-      if (fb != 0.0) bacc += (double)pc[dvp + e] * fb;
+  for (int e0 = 0; e0 < dv; e0 += 32 * kElems) {
+    // ---- hop B (vectors): cached acc and every split's acc slice, all in flight together ----
+    D aacc[kElems];
+#pragma unroll
+    for (int k = 0; k < kElems; ++k) {
+      const int e = e0 + lane + 32 * k;
+      aacc[k] = (use && e < dv) ? (D)racc[cslot * dv + e] : (D)0;
     }
-    double aacc = use ? (double)racc[cslot * dv + e] : 0.0;
-    // merge keeps an empty side's partner bit-exact (weight exp(0) == 1)
-    double pre = (La == -CUDART_INF) ? pacc : (Lp == -CUDART_INF ? aacc : aacc * wa + pacc * wp);
-    double full = (Lpre == -CUDART_INF) ? bacc : (Lb == -CUDART_INF ? pre : pre * wpre + bacc * wb);
-    out[(int64_t)bh * dv + e] = (S)full;
-    if (!full_mode) {
-      if (p.cached_acc) static_cast<S*>(p.cached_acc)[(int64_t)bh * dv + e] = (S)aacc;
-      double ring_v = pre;
-      if (do_remove) ring_v = (Lrem == -CUDART_INF) ? 0.0 : full * wr_full - bacc * wr_band;
-      racc_w[wslot * dv + e] = (S)ring_v;
+    M pacc[kElems] = {0, 0, 0, 0}, bacc[kElems] = {0, 0, 0, 0};
+    const M Lpm = (M)Lp, Lbm = (M)Lb;
+    for (int cb = 0; cb < ch.n; cb += kSplits) {
+      A xp[kSplits][kElems], xb[kSplits][kElems];
+      M wpc[kSplits], wbc[kSplits];
+#pragma unroll
+      for (int i = 0; i < kSplits; ++i) {
+        const int c = cb + i;
+        const bool ok = c < ch.n;
+        const A* row = pbase + (int64_t)c * cstride;
+#pragma unroll
+        for (int k = 0; k < kElems; ++k) {
+          const int e = e0 + lane + 32 * k;
+          xp[i][k] = (ok && e < dv) ? __ldg(row + e) : (A)0;
+          xb[i][k] = (ok && e < dv) ? __ldg(row + dvp + e) : (A)0;
+        }
+        const M l1 = cb == 0 ? (M)lse_p[i] : (ok ? (M)__ldg(row + dv) : neg_inf<M>());
+        const M l2 = cb == 0 ? (M)lse_b[i] : (ok ? (M)__ldg(row + dvp + dv) : neg_inf<M>());
+        wpc[i] = (l1 == neg_inf<M>() || Lp == NINF) ? (M)0 : fexp(l1 - Lpm);
+        wbc[i] = (l2 == neg_inf<M>() || Lb == NINF) ? (M)0 : fexp(l2 - Lbm);
+      }
+#pragma unroll
+      for (int i = 0; i < kSplits; ++i)
+#pragma unroll
+        for (int k = 0; k < kElems; ++k) {
+          pacc[k] += (M)xp[i][k] * wpc[i];
+          bacc[k] += (M)xb[i][k] * wbc[i];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kElems; ++k) {
+      const int e = e0 + lane + 32 * k;
+      if (e >= dv) continue;
+      // merge keeps an empty side's partner bit-exact (weight exp(0) == 1)
+      const D pk = (D)pacc[k], bk = (D)bacc[k];
+      const D pre = (La == NINF) ? pk : (Lp == NINF ? aacc[k] : aacc[k] * wa + pk * wp);
+      const D full = (Lpre == NINF) ? bk : (Lb == NINF ? pre : pre * wpre + bk * wb);
+      out[(int64_t)bh * dv + e] = (S)full;
+      if (!full_mode) {
+        if (p.cached_acc) static_cast<S*>(p.cached_acc)[(int64_t)bh * dv + e] = (S)aacc[k];
+        D ring_v = pre;
+        if (do_remove) ring_v = (Lrem == NINF) ? (D)0 : full * wr_full - bk * wr_band;
+        racc_w[wslot * dv + e] = (S)ring_v;
+      }
     }
   }
-  __syncthreads();  // cached summary fully read before the same slot may be overwritten
-  if (!full_mode) {
-    for (int k = threadIdx.x; k < d; k += blockDim.x)
-      rq[wslot * d + k] = from_f64<kv_t>(load_in(p.q_pre, (int64_t)bh * d + k, p.in_dtype));
+  if (!full_mode) {  // every lane read its cached slice above, before this slot can be overwritten
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kElems; ++k) {
+      const int e = lane + 32 * k;
+      if (e < d) rq[wslot * d + e] = from_f64<kv_t>(qv[k]);
+    }
+    for (int e = lane + 32 * kElems; e < d; e += 32)  // d > 128
+      rq[wslot * d + e] = from_f64<kv_t>(load_in(p.q_pre, (int64_t)bh * d + e, p.in_dtype));
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     static_cast<S*>(p.full_lse)[bh] = (S)Lfull;
     if (!full_mode) {
-      double lse_store = do_remove ? Lrem : Lpre;
+      const D lse_store = do_remove ? Lrem : Lpre;
       static_cast<S*>(p.ring_lse)[wslot] = (S)lse_store;
-      static_cast<S*>(p.band_mass)[bh] = (S)(bcount > 0 ? exp(Lb - Lfull) : 0.0);
+      static_cast<S*>(p.band_mass)[bh] = (S)(bcount > 0 ? fexp(Lb - Lfull) : (D)0);
       if (p.cached_lse) static_cast<S*>(p.cached_lse)[bh] = (S)La;
       if (p.fallbacks) p.fallbacks[bh] = fell_back;
     }
@@ -182,7 +225,7 @@ template <int MODE>
 cudaError_t launch_complete(const MacDecodeParams& p, cudaStream_t st, int full_mode) {
   Workspace w = workspace_layout(p);
   char* ws = static_cast<char*>(p.workspace);
-  complete_kernel<MODE><<<p.batch * p.n_q_heads, 128, 2 * sizeof(double) * p.max_chunks, st>>>(
+  complete_kernel<MODE><<<(p.batch * p.n_q_heads + 3) / 4, 128, 0, st>>>(
       p, reinterpret_cast<const int32_t*>(ws + w.mpos_off),
       reinterpret_cast<const typename Traits<MODE>::acc_t*>(ws + w.part_off), full_mode);
   return cudaGetLastError();
