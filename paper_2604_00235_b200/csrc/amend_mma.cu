@@ -21,12 +21,17 @@
 // with an atomic counter (dynamic load balance across heterogeneous spans,
 // the paper's K2 balancing).  A warp streams its item in
 // 16-token sub-tiles (one KV page for page_size % 16 == 0) with 16-byte
-// cp.async into an XOR-swizzled 3-stage ring (conflict-free ldmatrix).  The
-// piece -> band switch happens in-stream: the piece partial is written out
-// and the online-softmax state reset without draining the pipeline.
+// cp.async into an XOR-swizzled 4-stage ring (conflict-free ldmatrix) and
+// consumes them two at a time: a 32-token step keeps 8 independent QK
+// accumulator chains and 32 PV MMAs in flight, which is what a warp needs to
+// cover tensor-core and shuffle latency at ~7 warps per SM (measured with
+// %globaltimer traces: 16-token steps left warps compute-latency bound).
+// The piece -> band switch happens in-stream: the piece partial is written
+// out and the online-softmax state reset without draining the pipeline.
+#include <stdio.h>
 #include <stdlib.h>
 
-#include "common.cuh"
+#include "complete.cuh"
 
 namespace mac {
 
@@ -82,44 +87,61 @@ struct State {
   }
 };
 
-// fold one sub-tile's logits (this lane: 4 tokens of head `row`) into the state and accumulate P V
+// fold one 32-token step (two 16-token sub-tiles; this lane: 8 tokens of head `row`)
+// into the online-softmax state and accumulate P V.  vs1 == 0: second sub-tile absent.
 __device__ __forceinline__ void softmax_pv(State& S, const float* l_in, const int* tok, int lo, int hi,
-                                           uint32_t vs, int lane) {
-  float l[4];
+                                           uint32_t vs0, uint32_t vs1, int lane) {
+  float l[8];
   float mx = -CUDART_INF_F;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < 8; ++e) {
     l[e] = (tok[e] >= lo && tok[e] <= hi) ? l_in[e] : -CUDART_INF_F;
     mx = fmaxf(mx, l[e]);
   }
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
   const float Mn = fmaxf(S.M, mx);
-  float pv[4] = {0.f, 0.f, 0.f, 0.f};
+  float pv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float alpha = 1.f;
   if (Mn != -CUDART_INF_F) {
     alpha = exp2f(S.M - Mn);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) pv[e] = exp2f(l[e] - Mn);
+    for (int e = 0; e < 8; ++e) pv[e] = exp2f(l[e] - Mn);
   }
   S.M = Mn;
-  S.Z = S.Z * alpha + ((pv[0] + pv[1]) + (pv[2] + pv[3]));
+  S.Z = S.Z * alpha + (((pv[0] + pv[1]) + (pv[2] + pv[3])) + ((pv[4] + pv[5]) + (pv[6] + pv[7])));
+  // rescale only when some row's running max moved (warp-uniform test)
+  if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-  for (int nt = 0; nt < 16; ++nt) {
-    S.o[nt][0] *= alpha; S.o[nt][1] *= alpha; S.o[nt][2] *= alpha; S.o[nt][3] *= alpha;
+    for (int nt = 0; nt < 16; ++nt) {
+      S.o[nt][0] *= alpha; S.o[nt][1] *= alpha; S.o[nt][2] *= alpha; S.o[nt][3] *= alpha;
+    }
   }
-  float h0, lo0, h1, lo1, h2, lo2, h3, lo3;
-  split_bf16(pv[0], h0, lo0); split_bf16(pv[1], h1, lo1);
-  split_bf16(pv[2], h2, lo2); split_bf16(pv[3], h3, lo3);
-  const uint32_t pa[4] = {pack_bf16(h0, h1), pack_bf16(lo0, lo1), pack_bf16(h2, h3), pack_bf16(lo2, lo3)};
+  uint32_t pa[2][4];
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+    float h0, lo0, h1, lo1, h2, lo2, h3, lo3;
+    split_bf16(pv[4 * kk + 0], h0, lo0); split_bf16(pv[4 * kk + 1], h1, lo1);
+    split_bf16(pv[4 * kk + 2], h2, lo2); split_bf16(pv[4 * kk + 3], h3, lo3);
+    pa[kk][0] = pack_bf16(h0, h1);
+    pa[kk][1] = pack_bf16(lo0, lo1);
+    pa[kk][2] = pack_bf16(h2, h3);
+    pa[kk][3] = pack_bf16(lo2, lo3);
+  }
   const int mi = lane >> 3, ii = lane & 7;
   const int trow = ((mi & 1) << 3) + ii;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     uint32_t b0, b1, b2, b3;
-    ldsm_x4_t(vs + swz(trow, 2 * j + (mi >> 1)), b0, b1, b2, b3);
-    mma16816(S.o[2 * j], pa, b0, b1);
-    mma16816(S.o[2 * j + 1], pa, b2, b3);
+    ldsm_x4_t(vs0 + swz(trow, 2 * j + (mi >> 1)), b0, b1, b2, b3);
+    mma16816(S.o[2 * j], pa[0], b0, b1);
+    mma16816(S.o[2 * j + 1], pa[0], b2, b3);
+    if (vs1) {
+      uint32_t c0, c1, c2, c3;
+      ldsm_x4_t(vs1 + swz(trow, 2 * j + (mi >> 1)), c0, c1, c2, c3);
+      mma16816(S.o[2 * j], pa[1], c0, c1);
+      mma16816(S.o[2 * j + 1], pa[1], c2, c3);
+    }
   }
 }
 
@@ -147,7 +169,15 @@ bool amend_mma_supported(const MacDecodeParams& p) {
 }
 
 template <int ST, int MINB>  // cp.async stages per warp, min resident warps per SM (register budget)
-__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) {
+__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, int complete_mode) {
+  // programmatic dependent launch: wait for the front kernel's plan before touching it
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#ifdef MAC_TRACE
+  unsigned long long tr_start, tr_now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
+  int tr_items = 0, tr_sub = 0;
+  unsigned long long tr_first = 0, tr_wait = 0;
+#endif
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x;
   const int Hkv = p.n_kv_heads, Hq = p.n_q_heads, g = Hq / Hkv, r = p.band, ps = p.page_size;
@@ -161,23 +191,40 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
   const int* mpos = ws_ptr<const int>(p, w.mpos_off);
   const float* qrot = ws_ptr<const float>(p, w.qrot_off);
   float* part = ws_ptr<float>(p, w.part_off);
+  unsigned int* gdone = ws_ptr<unsigned int>(p, w.gdone_off);
+  const int* plan_n = ws_ptr<const int>(p, w.pn_off);
   const __nv_bfloat16* kc = static_cast<const __nv_bfloat16*>(p.k_cache);
   const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(p.v_cache);
-  const unsigned n_items = __ldcg(ctr);
+  // Every per-item scalar is passed through __reduce_max_sync: REDUX lands in a uniform
+  // register, so ptxas can prove the warp converged and the shuffles stay plain SHFL
+  // (values only known to be equal across lanes otherwise compile to slow
+  // WARPSYNC.COLLECTIVE sequences).
+  const unsigned n_items = __reduce_max_sync(0xffffffffu, __ldcg(ctr));
 
   // the next item's index and plan entry are fetched one item ahead, so the
   // atomic and the list load are off the critical path after the first item
   unsigned next = 0;
   if (lane == 0) next = atomicAdd(ctr + 1, 1u);
-  next = __shfl_sync(0xffffffffu, next, 0);
+  next = __reduce_max_sync(0xffffffffu, next);
   int4 next_it = next < n_items ? list[next] : make_int4(0, 0, 0, 0);
+#ifdef MAC_TRACE
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_now));
+  tr_first = tr_now - tr_start;
+#endif
   for (;;) {
     const unsigned item = next;
     if (item >= n_items) break;
+#ifdef MAC_TRACE
+    ++tr_items;
+#endif
     const int4 it = next_it;
-    if (lane == 0) next = atomicAdd(ctr + 1, 1u);
-    next = __shfl_sync(0xffffffffu, next, 0);
-    const int grp = it.x, c = it.y, t0 = it.z, t1 = it.w;
+    unsigned nx = 0;
+    if (lane == 0) nx = atomicAdd(ctr + 1, 1u);
+    next = __reduce_max_sync(0xffffffffu, nx);
+    const int grp = (int)__reduce_max_sync(0xffffffffu, (unsigned)it.x);
+    const int c = (int)__reduce_max_sync(0xffffffffu, (unsigned)it.y);
+    const int t0 = (int)__reduce_max_sync(0xffffffffu, (unsigned)it.z);
+    const int t1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)it.w);
     const int b = grp / Hkv, kvh = grp % Hkv;
     const int nsub = ((t1 - t0) >> 4) + 1;
     // page rows of the item's sub-tiles, 32 at a time (lane j holds sub-tile 32*blk + j),
@@ -215,7 +262,7 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
       cp_commit();
     }
     if (next < n_items) next_it = list[next];
-    const int m = mpos[b];
+    const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)mpos[b]);
     const int cpos = m - r;
     const int lo_h = row < g ? plan_lo[b * Hq + kvh * g + row] : (1 << 30);
     // Q fragments (hi rows 0..7, lo rows 8..15), 8 k-steps
@@ -245,38 +292,74 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
     bool in_band = false;
     const int lo_piece = max(lo_h, t0), hi_piece = min(t1, cpos);
     const int lo_band = max(lo_h, max(t0, cpos + 1));
-    for (int j = 0; j < nsub; ++j) {
-      const int stage = j % ST;
-      cp_wait<ST - 1>();
+#ifdef MAC_TRACE
+    tr_sub += nsub;
+#endif
+    // 32-token steps: sub-tiles 2jp and 2jp+1 (stages (2jp) % ST and (2jp+1) % ST)
+    const int nstep = (nsub + 1) >> 1;
+    for (int jp = 0; jp < nstep; ++jp) {
+      const int j0 = 2 * jp;
+      const bool has1 = j0 + 1 < nsub;
+#ifdef MAC_TRACE
+      unsigned long long tw0, tw1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw0));
+#endif
+      cp_wait<ST - 2>();
       __syncwarp();
-      const int ts = t0 + (j << 4);
-      const uint32_t ks_ = sm + stage * 2 * TILE_BYTES, vs_ = ks_ + TILE_BYTES;
-      float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#ifdef MAC_TRACE
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw1));
+      tr_wait += tw1 - tw0;
+#endif
+      const int ts = t0 + (jp << 5);
+      const uint32_t ks0 = sm + (j0 % ST) * 2 * TILE_BYTES, vs0 = ks0 + TILE_BYTES;
+      const uint32_t ks1 = sm + ((j0 + 1) % ST) * 2 * TILE_BYTES, vs1 = ks1 + TILE_BYTES;
+      // S = Q K^T for 4 n-tiles (32 tokens); even/odd k-steps accumulate separately
+      float s[4][2][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) s[nt][h2][0] = s[nt][h2][1] = s[nt][h2][2] = s[nt][h2][3] = 0.f;
       {
         const int mi = lane >> 3, ii = lane & 7;
         const int trow = ((mi >> 1) << 3) + ii;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           uint32_t b0, b1, b2, b3;
-          ldsm_x4(ks_ + swz(trow, 2 * ks + (mi & 1)), b0, b1, b2, b3);
-          mma16816(s0, qa[ks], b0, b1);
-          mma16816(s1, qa[ks], b2, b3);
+          ldsm_x4(ks0 + swz(trow, 2 * ks + (mi & 1)), b0, b1, b2, b3);
+          mma16816(s[0][ks & 1], qa[ks], b0, b1);
+          mma16816(s[1][ks & 1], qa[ks], b2, b3);
+          if (has1) {
+            uint32_t c0, c1, c2, c3;
+            ldsm_x4(ks1 + swz(trow, 2 * ks + (mi & 1)), c0, c1, c2, c3);
+            mma16816(s[2][ks & 1], qa[ks], c0, c1);
+            mma16816(s[3][ks & 1], qa[ks], c2, c3);
+          }
         }
       }
-      const float l[4] = {(s0[0] + s0[2]) * scale2, (s0[1] + s0[3]) * scale2, (s1[0] + s1[2]) * scale2,
-                          (s1[1] + s1[3]) * scale2};
-      const int tok[4] = {ts + q4 * 2, ts + q4 * 2 + 1, ts + 8 + q4 * 2, ts + 9 + q4 * 2};
-      if (ts <= hi_piece) softmax_pv(S, l, tok, lo_piece, hi_piece, vs_, lane);
-      if (ts + 15 > cpos && max(ts, cpos + 1) <= t1) {
+      float l[8];
+      int tok[8];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        l[2 * nt] = ((s[nt][0][0] + s[nt][1][0]) + (s[nt][0][2] + s[nt][1][2])) * scale2;
+        l[2 * nt + 1] = ((s[nt][0][1] + s[nt][1][1]) + (s[nt][0][3] + s[nt][1][3])) * scale2;
+        tok[2 * nt] = ts + nt * 8 + q4 * 2;
+        tok[2 * nt + 1] = ts + nt * 8 + q4 * 2 + 1;
+      }
+      const int hi_band = has1 ? t1 : min(t1, ts + 15);
+      if (ts <= hi_piece) softmax_pv(S, l, tok, lo_piece, has1 ? hi_piece : min(hi_piece, ts + 15), vs0,
+                                     has1 ? vs1 : 0u, lane);
+      if (ts + 31 > cpos && max(ts, cpos + 1) <= t1) {
         if (!in_band) {
           write_partial(S, out, 0, row, q4, g);
           S.reset();
           in_band = true;
         }
-        softmax_pv(S, l, tok, lo_band, t1, vs_, lane);
+        softmax_pv(S, l, tok, lo_band, hi_band, vs0, has1 ? vs1 : 0u, lane);
       }
       __syncwarp();
-      if (j + ST < nsub) issue(j + ST, stage);
+      if (j0 + ST < nsub) issue(j0 + ST, j0 % ST);
+      cp_commit();
+      if (j0 + 1 + ST < nsub) issue(j0 + 1 + ST, (j0 + 1) % ST);
       cp_commit();
     }
     cp_wait<0>();
@@ -285,12 +368,35 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
       S.reset();
     }
     write_partial(S, out, 1, row, q4, g);
+    if (complete_mode) {
+      // the warp that lands a group's last split completes the group's heads (K3 fused)
+      unsigned last = 0;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(gdone + grp, 1u);
+        last = prev + 1 == (unsigned)plan_n[grp];
+        if (last) gdone[grp] = 0u;
+      }
+      last = __reduce_max_sync(0xffffffffu, last);
+      if (last) {
+        __threadfence();
+        for (int j = 0; j < g; ++j) complete_head<MAC_MODE_BF16>(p, b * Hq + kvh * g + j, complete_mode == 2);
+      }
+    }
   }
+#ifdef MAC_TRACE
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_now));
+  if (lane == 0 && (blockIdx.x % 97 == 0))
+    printf("TRACE amend cta=%d sm_items=%d subtiles=%d first_fetch_ns=%llu wait_ns=%llu total_ns=%llu start=%llu\n",
+           blockIdx.x, tr_items, tr_sub, tr_first, tr_wait, tr_now - tr_start, tr_start);
+#endif
   // last warp out resets the work counter for the next step
   if (lane == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(ctr + 2, 1u);
     if (prev == gridDim.x - 1) {
+      if (complete_mode) ctr[0] = 0u;  // fused complete: the work list is fully consumed
       ctr[1] = 0u;
       ctr[2] = 0u;
     }
@@ -299,16 +405,16 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
 
 // Variants (stages, min warps per SM); MAC_AMEND_VARIANT selects one (development knob).
 struct AmendVariant {
-  void (*fn)(MacDecodeParams);
+  void (*fn)(MacDecodeParams, int);
   int smem;
 };
 static const AmendVariant kAmendVariants[] = {
-    {amend_mma_kernel<3, 8>, 3 * 2 * TILE_BYTES},  {amend_mma_kernel<2, 12>, 2 * 2 * TILE_BYTES},
-    {amend_mma_kernel<2, 10>, 2 * 2 * TILE_BYTES}, {amend_mma_kernel<3, 9>, 3 * 2 * TILE_BYTES},
-    {amend_mma_kernel<4, 7>, 4 * 2 * TILE_BYTES},  {amend_mma_kernel<2, 14>, 2 * 2 * TILE_BYTES},
+    {amend_mma_kernel<4, 7>, 4 * 2 * TILE_BYTES},
+    {amend_mma_kernel<6, 4>, 6 * 2 * TILE_BYTES},
+    {amend_mma_kernel<2, 8>, 2 * 2 * TILE_BYTES},
 };
 
-cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st) {
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, int complete_mode) {
   static int grid_full = 0, vi = 0;
   if (!grid_full) {
     const char* env = getenv("MAC_AMEND_VARIANT");
@@ -326,8 +432,18 @@ cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st) {
   const AmendVariant& v = kAmendVariants[vi];
   const long cap = (long)p.batch * p.n_kv_heads * p.max_chunks;
   const int grid = (int)(grid_full < cap ? grid_full : cap);
-  v.fn<<<grid, 32, v.smem, st>>>(p);
-  return cudaGetLastError();
+  // programmatic dependent launch: the grid is set up while the front kernel drains
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = v.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, v.fn, p, complete_mode);
 }
 
 }  // namespace mac

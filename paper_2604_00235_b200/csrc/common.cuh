@@ -168,6 +168,8 @@ struct Workspace {
   size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
   size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
   size_t ctr_off;    // [4] u32      work-list length, amend work counter, amend done counter
+  size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
+  size_t pn_off;     // [B*Hkv] i32  splits planned for the group
   size_t mpos_off;   // [B] i32      position m of this step
   size_t lo_off;     // [B*Hq] i32   first token each head reads (plan)
   size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp, c, t0, t1}
@@ -185,7 +187,9 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.marr_off = align256(w.mkey_off + 8 * rows);
   w.gcnt_off = align256(w.marr_off + 4 * rows);
   w.ctr_off = align256(w.gcnt_off + 4 * groups);
-  w.mpos_off = align256(w.ctr_off + 16);
+  w.gdone_off = align256(w.ctr_off + 16);
+  w.pn_off = align256(w.gdone_off + 4 * groups);
+  w.mpos_off = align256(w.pn_off + 4 * groups);
   w.lo_off = align256(w.mpos_off + 4 * (size_t)p.batch);
   w.list_off = align256(w.lo_off + 4 * rows);
   w.qrot_off = align256(w.list_off + 16 * groups * p.max_chunks);
@@ -208,8 +212,9 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
   unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
   int4* list = ws_ptr<int4>(p, w.list_off);
   const unsigned cap = (unsigned)(p.batch * p.n_kv_heads * p.max_chunks);
-  const unsigned base = atomicAdd(ctr, (unsigned)ch.n);
   const int grp = b * p.n_kv_heads + kvh;
+  ws_ptr<int>(p, w.pn_off)[grp] = ch.n;
+  const unsigned base = atomicAdd(ctr, (unsigned)ch.n);
   for (int c = 0; c < ch.n; ++c) {
     if (base + c >= cap) break;  // cannot happen when every step is completed
     const int t0 = start + c * ch.len;

@@ -19,14 +19,14 @@
 // arrival count decides the head (decide_head) and resets key and counter to
 // zero for the next step (graph-replay safe).  The step's KV appends (one
 // warp per (request, kv head)) ride in the same launch.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mac {
 
 namespace {
 constexpr int kThreads = 256;
-constexpr int kRowsPerCta = 128;
-constexpr int kLoads = kRowsPerCta / 16;  // per thread: 8 warps x 2 rows per load instruction
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
@@ -92,8 +92,11 @@ __device__ void append_warp(const MacDecodeParams& p, int idx, int rotate_only, 
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 5) front_bf16_d128_kernel(MacDecodeParams p, int n_match, int do_append,
-                                                                      int rotate_only, int plan) {
+template <int kRowsPerCta, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(MacDecodeParams p, int n_match,
+                                                                               int do_append, int rotate_only,
+                                                                               int plan) {
+  constexpr int kLoads = kRowsPerCta / 16;  // per thread: 8 warps x 2 rows per load instruction
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the first n_append CTAs append (one warp per (request, kv head)); they are
   // scheduled first so their latency hides under the ring stream
@@ -101,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 5) front_bf16_d128_kernel(MacDecodeP
   if ((int)blockIdx.x < n_append) {
     const int i = blockIdx.x * (kThreads / 32) + warp;
     if (i < p.batch * p.n_kv_heads) append_warp(p, i, rotate_only, plan);
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     return;
   }
   const int W = p.window;
@@ -152,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 5) front_bf16_d128_kernel(MacDecodeP
   __shared__ unsigned long long wkey[kThreads / 32];
   if (lane == 0) wkey[warp] = key;
   __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (tid != 0) return;
   for (int w = 1; w < kThreads / 32; ++w) key = wkey[w] > key ? wkey[w] : key;
   const Workspace ws = workspace_layout(p);
@@ -181,13 +186,31 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-// match CTAs (128 ring rows each) followed by append CTAs (8 warps, one (request, kv head) each)
+// Variants (ring rows per CTA, min CTAs per SM); MAC_FRONT_VARIANT selects one (development knob).
+struct FrontVariant {
+  void (*fn)(MacDecodeParams, int, int, int, int);
+  int rows;
+};
+static const FrontVariant kFrontVariants[] = {
+    {front_bf16_d128_kernel<128, 5>, 128}, {front_bf16_d128_kernel<64, 8>, 64},
+    {front_bf16_d128_kernel<256, 3>, 256}, {front_bf16_d128_kernel<64, 6>, 64},
+    {front_bf16_d128_kernel<128, 4>, 128}, {front_bf16_d128_kernel<32, 8>, 32},
+};
+
+// append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
 cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append,
                               int rotate_only, int plan) {
-  const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + kRowsPerCta - 1) / kRowsPerCta) : 0;
+  static int vi = -1;
+  if (vi < 0) {
+    const char* env = getenv("MAC_FRONT_VARIANT");
+    vi = env ? atoi(env) : 0;
+    if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
+  }
+  const FrontVariant& v = kFrontVariants[vi];
+  const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + v.rows - 1) / v.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;
-  front_bf16_d128_kernel<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan);
+  v.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan);
   return cudaGetLastError();
 }
 
