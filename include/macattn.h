@@ -23,6 +23,9 @@
  *                     (no append): the per-step fidelity oracle (engine.py:507-509)
  *   mac_merge_partials  log-domain merge of per-shard (acc, lse) partials
  *                     (attention.py:119-135 merge) for the KV-sharded miss path
+ *   mac_shard_partial / mac_shard_complete  decode_step split around the one
+ *                     cross-GPU exchange of the KV-sharded path (all-gather of
+ *                     per-shard (piece, band) summaries, then the merge)
  *
  * Conventions: plain device pointers and sizes, no allocation inside, every
  * launch is stream-ordered and graph-capturable (no host synchronisation).
@@ -39,7 +42,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 1
+#define MACATTN_ABI_VERSION 2
 
 /* storage modes: dtype of the K/V cache and the query ring; summaries are
  * f32 in MAC_MODE_F32/BF16 and f64 in MAC_MODE_F64 (engine.py:152-153 allows
@@ -77,6 +80,9 @@ typedef struct MacDecodeParams {
   int32_t max_chunks;    /* split-KV partial slots per (request, kv head) */
   int32_t min_chunk;     /* minimum tokens per split */
   int32_t kv_offset;     /* tokens of this request held by earlier KV shards (0 unless sharded) */
+  int32_t kv_limit;      /* tokens this KV shard holds (positions kv_offset+1 .. kv_offset+kv_limit);
+                            0: unbounded (the tail shard, or no sharding) */
+  int32_t n_shards;      /* partials in shard_parts (mac_shard_complete) */
   /* ---- match rule (matching.py:58-64, 141-175; engine.py:452-459) ----- */
   double thr_sq;         /* (sqrt(2d)(1 - tau_layer))^2 */
   int32_t delta_max;     /* <= 0: off */
@@ -113,6 +119,9 @@ typedef struct MacDecodeParams {
   void* cached_acc;           /* optional [B, Hq, d_v]: summary reused at p (NULL: not written) */
   void* cached_lse;           /* optional [B, Hq] */
   int32_t* fallbacks;         /* optional [B, Hq]: 1 when remove() fell back to the split prefix */
+  /* ---- KV-sharded miss path ------------------------------ */
+  void* shard_out;            /* [B, Hq, 2, d_v+1] this shard's (piece, band) partials: acc..., lse */
+  const void* shard_parts;    /* [n_shards, B, Hq, 2, d_v+1] every shard's partials, rank order */
   /* ---- scratch --------------------------------------------------------- */
   void* workspace;
   size_t workspace_bytes;
@@ -146,6 +155,14 @@ int mac_decode_step(const MacDecodeParams* p, void* stream);
 int mac_full_decode(const MacDecodeParams* p, void* stream);
 int mac_attend_full(const MacDecodeParams* p, void* stream);
 int mac_merge_partials(const MacMergeParams* p, void* stream);
+/* KV-sharded step, half 1: append (stored only by the shard holding position m),
+ * match, plan clamped to this shard's tokens, amend, and the per-head (piece,
+ * band) partials of this shard into shard_out.  Rings and seq_lens untouched. */
+int mac_shard_partial(const MacDecodeParams* p, void* stream);
+/* half 2, after the caller gathered every shard's shard_out into shard_parts:
+ * cached(p) (+) pieces (+) bands in rank order, output, rho, ring write-back,
+ * seq_lens advance.  Every shard computes the same result. */
+int mac_shard_complete(const MacDecodeParams* p, void* stream);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
@@ -34,6 +34,8 @@ EXPORTS = (
     "mac_full_decode",
     "mac_attend_full",
     "mac_merge_partials",
+    "mac_shard_partial",
+    "mac_shard_complete",
 )
 
 
@@ -53,6 +55,8 @@ class MacDecodeParams(C.Structure):
         ("max_chunks", C.c_int32),
         ("min_chunk", C.c_int32),
         ("kv_offset", C.c_int32),
+        ("kv_limit", C.c_int32),
+        ("n_shards", C.c_int32),
         ("thr_sq", C.c_double),
         ("delta_max", C.c_int32),
         ("match_space", C.c_int32),
@@ -85,6 +89,8 @@ class MacDecodeParams(C.Structure):
         ("cached_acc", C.c_void_p),
         ("cached_lse", C.c_void_p),
         ("fallbacks", C.c_void_p),
+        ("shard_out", C.c_void_p),
+        ("shard_parts", C.c_void_p),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
     ]
@@ -129,7 +135,7 @@ def load() -> C.CDLL:
     lib.mac_amend_variant.restype = C.c_int
     lib.mac_amend_variant.argtypes = [C.POINTER(MacDecodeParams)]
     for name in ("mac_append_kv", "mac_match", "mac_amend", "mac_complete", "mac_decode_step", "mac_full_decode",
-                 "mac_attend_full"):
+                 "mac_attend_full", "mac_shard_partial", "mac_shard_complete"):
         fn = getattr(lib, name)
         fn.restype = C.c_int
         fn.argtypes = [C.POINTER(MacDecodeParams), C.c_void_p]

@@ -59,10 +59,10 @@ __global__ void __launch_bounds__(128) amend_generic_kernel(MacDecodeParams p, c
       if (lo < lo_g) lo_g = lo;
     }
     const int lo_first = grid_start(lo_g, p.kv_offset);  // shard-local floor
-    const Chunking ch = chunking(m - lo_first + 1, p.max_chunks, p.min_chunk);
+    const Chunking ch = group_chunking(p, m, lo_g);
     if (c >= ch.n) continue;  // block-uniform
     const int t0 = lo_first + c * ch.len;
-    const int t1 = min(m, t0 + ch.len - 1);
+    const int t1 = min(shard_end(p, m), t0 + ch.len - 1);
     const int cpos = m - r;
 
     __syncthreads();  // previous item finished with shared memory

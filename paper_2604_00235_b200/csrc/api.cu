@@ -37,6 +37,7 @@ static int validate(const MacDecodeParams* p, bool need_ring) {
   if (need_ring && (!p->ring_q || !p->ring_acc || !p->ring_lse || !p->match_hit || !p->use_hit || !p->match_pos ||
                     !p->match_dist || !p->match_scanned || !p->band_mass))
     return MAC_ERR_NULL;
+  if (p->kv_limit < 0) return MAC_ERR_SHAPE;
   if (p->workspace_bytes < workspace_layout(*p).total) return MAC_ERR_WORKSPACE;
   return MAC_OK;
 }
@@ -48,7 +49,9 @@ enum : int {
   STAGE_COMPLETE = 8,       // merge, output, ring write-back
   STAGE_COMPLETE_FULL = 16, // merge and output only (full-attention modes)
   STAGE_ROTATE = 32,        // rotate q at m = seq_lens, no append
-  STAGE_PLAN_FULL = 64      // plan every group as [1, m] in the append stage
+  STAGE_PLAN_FULL = 64,     // plan every group as [1, m] in the append stage
+  STAGE_EXPORT = 128,       // this KV shard's (piece, band) partials -> shard_out
+  STAGE_SHARDS = 256        // merge the gathered shard partials, output, ring write-back
 };
 
 template <int MODE>
@@ -71,7 +74,7 @@ static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int mask)
   // the tensor-core amend completes each group in its tail when the step asks for
   // amend and complete together (mac_decode_step / mac_full_decode)
   static const int fuse_ok = getenv("MAC_FUSE_COMPLETE") ? atoi(getenv("MAC_FUSE_COMPLETE")) : 0;  // measured slower
-  const int fused = (fuse_ok && fast_amend && (mask & STAGE_AMEND))
+  const int fused = (fuse_ok && fast_amend && (mask & STAGE_AMEND) && !(mask & STAGE_EXPORT))
                         ? ((mask & STAGE_COMPLETE) ? 1 : ((mask & STAGE_COMPLETE_FULL) ? 2 : 0))
                         : 0;
   if (mask & STAGE_AMEND) {
@@ -82,6 +85,8 @@ static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int mask)
   if (!fused) {
     if (mask & STAGE_COMPLETE) { e = launch_complete<MODE>(p, st, 0); if (e) return e; }
     if (mask & STAGE_COMPLETE_FULL) { e = launch_complete<MODE>(p, st, 1); if (e) return e; }
+    if (mask & STAGE_EXPORT) { e = launch_complete<MODE>(p, st, 2); if (e) return e; }
+    if (mask & STAGE_SHARDS) { e = launch_complete<MODE>(p, st, 3); if (e) return e; }
   }
   return e;
 }
@@ -144,6 +149,19 @@ int mac_attend_full(const MacDecodeParams* p, void* stream) {
   q.force_miss = 1;
   q.band = 0;
   return dispatch(&q, stream, STAGE_ROTATE | STAGE_PLAN_FULL | STAGE_AMEND | STAGE_COMPLETE_FULL, false);
+}
+
+int mac_shard_partial(const MacDecodeParams* p, void* stream) {
+  if (!p) return MAC_ERR_NULL;
+  if (!p->shard_out) return MAC_ERR_NULL;
+  return dispatch(p, stream, STAGE_APPEND | STAGE_MATCH | STAGE_AMEND | STAGE_EXPORT, true);
+}
+
+int mac_shard_complete(const MacDecodeParams* p, void* stream) {
+  if (!p) return MAC_ERR_NULL;
+  if (!p->shard_parts) return MAC_ERR_NULL;
+  if (p->n_shards < 1) return MAC_ERR_SHAPE;
+  return dispatch(p, stream, STAGE_SHARDS, true);
 }
 
 int mac_merge_partials(const MacMergeParams* p, void* stream) {

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
   const int t_local = m - p.kv_offset;        // position inside this shard's cache
   if (kvh == 0 && threadIdx.x == 0) mpos[b] = m;
-  const bool store_kv = !rotate_only && t_local >= 1;
+  const bool store_kv = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
   int64_t row = 0;
   if (store_kv) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
   kv_t* kc = static_cast<kv_t*>(p.k_cache);

@@ -99,6 +99,14 @@ __device__ __forceinline__ float logaddexp(float a, float b) {
 __device__ __forceinline__ float fexpm1(float x) { return expm1f(x); }
 __device__ __forceinline__ double fexpm1(double x) { return expm1(x); }
 
+// gpu-scope acquire-release fetch-add: orders this thread's earlier writes before
+// the increment and later reads after it (replaces a fence + atomicAdd pair)
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -150,6 +158,15 @@ __host__ __device__ __forceinline__ int grid_start(int lo_g, int kv_offset) {
   return local + kv_offset;
 }
 
+// last position this KV shard holds for a step at position m (kv_limit 0: unbounded)
+__host__ __device__ __forceinline__ int shard_end(const MacDecodeParams& p, int m) {
+  return (p.kv_limit > 0 && p.kv_offset + p.kv_limit < m) ? p.kv_offset + p.kv_limit : m;
+}
+// the split grid of a GQA group over [grid_start(lo_g), shard_end(m)] (plan, amend and complete agree)
+__host__ __device__ __forceinline__ Chunking group_chunking(const MacDecodeParams& p, int m, int lo_g) {
+  return chunking(shard_end(p, m) - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks, p.min_chunk);
+}
+
 // physical row of token t (1-based, local to this KV shard) in a paged cache
 __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table, int pages_per_seq,
                                           int b, int t, int page_size, int n_kv, int kvh) {
@@ -167,7 +184,8 @@ struct Workspace {
   size_t mkey_off;   // [B*Hq] u64   complemented packed (dist, pos) match key
   size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
   size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
-  size_t ctr_off;    // [4] u32      work-list length, amend work counter, amend done counter
+  size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter, 2 amend done counter,
+                     //              3 front item counter, 4 front done counter
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  splits planned for the group
   size_t mpos_off;   // [B] i32      position m of this step
@@ -187,7 +205,7 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.marr_off = align256(w.mkey_off + 8 * rows);
   w.gcnt_off = align256(w.marr_off + 4 * rows);
   w.ctr_off = align256(w.gcnt_off + 4 * groups);
-  w.gdone_off = align256(w.ctr_off + 16);
+  w.gdone_off = align256(w.ctr_off + 64);
   w.pn_off = align256(w.gdone_off + 4 * groups);
   w.mpos_off = align256(w.pn_off + 4 * groups);
   w.lo_off = align256(w.mpos_off + 4 * (size_t)p.batch);
@@ -207,7 +225,8 @@ template <typename T> __host__ __device__ __forceinline__ T* ws_ptr(const MacDec
 // load-balancer plan, built on the device with no host synchronisation).
 __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g) {
   const int start = grid_start(lo_g, p.kv_offset);
-  const Chunking ch = chunking(m - start + 1, p.max_chunks, p.min_chunk);
+  const int end = shard_end(p, m);
+  const Chunking ch = group_chunking(p, m, lo_g);
   const Workspace w = workspace_layout(p);
   unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
   int4* list = ws_ptr<int4>(p, w.list_off);
@@ -218,7 +237,7 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
   for (int c = 0; c < ch.n; ++c) {
     if (base + c >= cap) break;  // cannot happen when every step is completed
     const int t0 = start + c * ch.len;
-    const int t1 = min(m, t0 + ch.len - 1);
+    const int t1 = min(end, t0 + ch.len - 1);
     list[base + c] = make_int4(grp, c, t0, t1);
   }
 }
@@ -244,13 +263,11 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
   const Workspace w = workspace_layout(p);
   int* lo = ws_ptr<int>(p, w.lo_off);
   lo[bh] = head_lo(use, pp, p.band);
-  __threadfence();
   const int b = bh / Hq, h = bh % Hq, kvh = h / g;
   unsigned int* gcnt = ws_ptr<unsigned int>(p, w.gcnt_off);
-  const unsigned prev = atomicAdd(gcnt + b * Hkv + kvh, 1u);
+  const unsigned prev = atom_add_acq_rel(gcnt + b * Hkv + kvh, 1u);
   if (prev == (unsigned)g - 1) {
     gcnt[b * Hkv + kvh] = 0u;
-    __threadfence();
     int lo_g = m;
     for (int j = 0; j < g; ++j) {
       const int l = __ldcg(lo + b * Hq + kvh * g + j);

@@ -20,12 +20,20 @@ namespace mac {
 constexpr int kElems = 4;   // d_v elements per lane per pass (d_v <= 128 in one pass)
 constexpr int kSplits = 8;  // splits whose partials are loaded in one batch
 
+// Modes of complete_head:
+enum : int {
+  COMPLETE_RING = 0,    // decode step: merge, output, rho, ring write-back, seq_lens advance
+  COMPLETE_FULL = 1,    // full-attention decode: merge and output only
+  COMPLETE_EXPORT = 2,  // KV shard: this shard's (piece, band) summaries -> shard_out
+  COMPLETE_SHARDS = 3   // KV-sharded step: partials are the gathered shard_parts; as COMPLETE_RING
+};
+
 // One warp per (request, q head), 4 heads per CTA.  The merge is latency-bound,
 // so memory is touched in two hops: (A) the step's scalars, (B) every partial,
 // the cached ring summary and the query row, all issued before any use; the
 // algebra then runs from registers.
 template <int MODE>
-__device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, int full_mode) {
+__device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, int mode) {
   using kv_t = typename Traits<MODE>::kv_t;
   using A = typename Traits<MODE>::acc_t;
   using S = typename Traits<MODE>::sum_t;
@@ -40,6 +48,7 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
   const int d = p.head_dim, dv = p.head_dim_v, W = p.window, r = p.band, dvp = dv + 1;
   const int* plan_lo = ws_ptr<const int>(p, wsl.lo_off);
   const D NINF = neg_inf<D>();
+  const bool full_mode = mode == COMPLETE_FULL || mode == COMPLETE_EXPORT;  // no ring traffic
 
   // ---- hop A: scalars of this step ----
   const int m = mpos[b];
@@ -60,17 +69,22 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
   for (int o = 16; o > 0; o >>= 1) lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, o));
   lo_g = min(lo_g, m);
   const int pp = use ? pp_raw : -1;
-  const Chunking ch = chunking(m - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks, p.min_chunk);
+  Chunking ch = group_chunking(p, m, lo_g);
   const int cpos = m - r;
   const int grp = b * Hkv + kvh;
   const A* pbase = part + ((int64_t)grp * p.max_chunks * g + hl) * 2 * dvp;
-  const int cstride = g * 2 * dvp;
+  int64_t cstride = (int64_t)g * 2 * dvp;
+  if (mode == COMPLETE_SHARDS) {  // one (piece, band) pair per shard, rank order
+    pbase = static_cast<const A*>(p.shard_parts) + (int64_t)bh * 2 * dvp;
+    cstride = (int64_t)p.batch * p.n_q_heads * 2 * dvp;
+    ch.n = p.n_shards;
+  }
   const S* racc = static_cast<const S*>(p.ring_acc);
   const S* rlse = static_cast<const S*>(p.ring_lse);
   const int64_t cslot = use ? (int64_t)bh * W + (pp - 1) % W : 0;
 
   // ---- hop B: cached summary + split lse values ----
-  const D La = use ? (D)rlse[cslot] : NINF;
+  const D La = (use && mode != COMPLETE_EXPORT) ? (D)rlse[cslot] : NINF;
   A lse_p[kSplits], lse_b[kSplits];
 #pragma unroll
   for (int i = 0; i < kSplits; ++i) {
@@ -149,7 +163,7 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
 #pragma unroll
     for (int k = 0; k < kElems; ++k) {
       const int e = e0 + lane + 32 * k;
-      aacc[k] = (use && e < dv) ? (D)racc[cslot * dv + e] : (D)0;
+      aacc[k] = (use && mode != COMPLETE_EXPORT && e < dv) ? (D)racc[cslot * dv + e] : (D)0;
     }
     M pacc[kElems] = {0, 0, 0, 0}, bacc[kElems] = {0, 0, 0, 0};
     const M Lpm = (M)Lp, Lbm = (M)Lb;
@@ -186,6 +200,12 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
       if (e >= dv) continue;
       // merge keeps an empty side's partner bit-exact (weight exp(0) == 1)
       const D pk = (D)pacc[k], bk = (D)bacc[k];
+      if (mode == COMPLETE_EXPORT) {
+        S* so = static_cast<S*>(p.shard_out) + (int64_t)bh * 2 * dvp;
+        so[e] = (S)pk;
+        so[dvp + e] = (S)bk;
+        continue;
+      }
       const D pre = (La == NINF) ? pk : (Lp == NINF ? aacc[k] : aacc[k] * wa + pk * wp);
       const D full = (Lpre == NINF) ? bk : (Lb == NINF ? pre : pre * wpre + bk * wb);
       out[(int64_t)bh * dv + e] = (S)full;
@@ -206,6 +226,14 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
     }
     for (int e = lane + 32 * kElems; e < d; e += 32)  // d > 128
       rq[wslot * d + e] = from_f64<kv_t>(load_in(p.q_pre, (int64_t)bh * d + e, p.in_dtype));
+  }
+  if (mode == COMPLETE_EXPORT) {
+    if (lane == 0) {
+      S* so = static_cast<S*>(p.shard_out) + (int64_t)bh * 2 * dvp;
+      so[dv] = (S)Lp;
+      so[dvp + dv] = (S)Lb;
+    }
+    return;
   }
   if (lane == 0) {
     static_cast<S*>(p.full_lse)[bh] = (S)Lfull;

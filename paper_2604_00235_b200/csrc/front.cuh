@@ -1,0 +1,90 @@
+// Shared pieces of the front (append + match + plan) kernels: the per-(request,
+// kv head) append warp and the cross-CTA argmin publication.
+#pragma once
+
+#include "common.cuh"
+
+namespace mac {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// append + RoPE for one (request, kv head) by one warp; optionally plan the group as "all heads miss"
+__device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, int rotate_only, int plan) {
+  const int lane = threadIdx.x & 31;
+  const int b = idx / p.n_kv_heads, kvh = idx % p.n_kv_heads;
+  const int g = p.n_q_heads / p.n_kv_heads;
+  const Workspace w = workspace_layout(p);
+  const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
+  if (kvh == 0 && lane == 0) ws_ptr<int>(p, w.mpos_off)[b] = m;
+  const int t_local = m - p.kv_offset;
+  const bool store = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
+  int64_t row = 0;
+  if (store) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
+  __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);
+  __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(p.v_cache);
+  float* qrot = ws_ptr<float>(p, w.qrot_off);
+  for (int j = lane; j < 64; j += 32) {
+    double s, c;
+    sincos((double)m * p.rope_freqs[j], &s, &c);
+    if (store) {
+      const int64_t ki = ((int64_t)b * p.n_kv_heads + kvh) * 128 + 2 * j;
+      const double x0 = load_in(p.k_pre, ki, p.in_dtype), x1 = load_in(p.k_pre, ki + 1, p.in_dtype);
+      __nv_bfloat162 kk;
+      kk.x = from_f64<__nv_bfloat16>(x0 * c - x1 * s);
+      kk.y = from_f64<__nv_bfloat16>(x0 * s + x1 * c);
+      reinterpret_cast<__nv_bfloat162*>(kc + row * 128)[j] = kk;
+    }
+    for (int hl = 0; hl < g; ++hl) {
+      const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
+      const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
+      reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+    }
+  }
+  if (store)
+    for (int e = lane; e < 128; e += 32)
+      vc[row * 128 + e] =
+          from_f64<__nv_bfloat16>(load_in(p.v_in, ((int64_t)b * p.n_kv_heads + kvh) * 128 + e, p.in_dtype));
+  if (plan && lane == 0) {
+    int* lo = ws_ptr<int>(p, w.lo_off);
+    for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;
+    plan_group(p, b, kvh, m, 1);
+  }
+}
+
+// Publication of one worker's best candidate (complemented packed key
+// ~(dist_bits << 32 | ~pos), 0 = nothing) for its (request, head), in two
+// halves so a streaming worker need not wait for the round trip: publish_key
+// returns the previous arrival count (consume it later); the worker that
+// brought the count to nsplit runs finish_decide, which decides the head
+// (decide_head) and returns key and counter to zero for the next step
+// (graph-replay safe).  Single thread.
+__device__ __forceinline__ unsigned publish_key(const MacDecodeParams& p, int bh, unsigned long long key) {
+  const Workspace ws = workspace_layout(p);
+  if (key) atomicMax(ws_ptr<unsigned long long>(p, ws.mkey_off) + bh, key);
+  return atom_add_acq_rel(ws_ptr<unsigned int>(p, ws.marr_off) + bh, 1u);
+}
+
+__device__ __forceinline__ void finish_decide(const MacDecodeParams& p, int bh, int m, int n_scan) {
+  const Workspace ws = workspace_layout(p);
+  const unsigned long long k3 = atomicExch(ws_ptr<unsigned long long>(p, ws.mkey_off) + bh, 0ull);
+  ws_ptr<unsigned int>(p, ws.marr_off)[bh] = 0u;
+  double bd = CUDART_INF;
+  int bp = -1;
+  if (k3) {
+    const unsigned long long raw = ~k3;
+    bd = (double)__uint_as_float((unsigned)(raw >> 32));
+    bp = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
+  }
+  decide_head(p, bh, m, n_scan, bp > 0, bd, bp);
+}
+
+__device__ __forceinline__ void publish_and_decide(const MacDecodeParams& p, int bh, int m, int n_scan, int nsplit,
+                                                   unsigned long long key) {
+  if (publish_key(p, bh, key) == (unsigned)nsplit - 1) finish_decide(p, bh, m, n_scan);
+}
+
+}  // namespace mac

@@ -21,18 +21,12 @@
 // warp per (request, kv head)) ride in the same launch.
 #include <stdlib.h>
 
-#include "common.cuh"
+#include "front.cuh"
 
 namespace mac {
 
 namespace {
 constexpr int kThreads = 256;
-
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
 
 __device__ __forceinline__ float dist8(const float* q, uint4 c) {
   float acc = 0.f;
@@ -48,48 +42,6 @@ __device__ __forceinline__ float dist8(const float* q, uint4 c) {
   return acc;
 }
 
-// append + RoPE for one (request, kv head) by one warp; optionally plan the group as "all heads miss"
-__device__ void append_warp(const MacDecodeParams& p, int idx, int rotate_only, int plan) {
-  const int lane = threadIdx.x & 31;
-  const int b = idx / p.n_kv_heads, kvh = idx % p.n_kv_heads;
-  const int g = p.n_q_heads / p.n_kv_heads;
-  const Workspace w = workspace_layout(p);
-  const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
-  if (kvh == 0 && lane == 0) ws_ptr<int>(p, w.mpos_off)[b] = m;
-  const int t_local = m - p.kv_offset;
-  const bool store = !rotate_only && t_local >= 1;
-  int64_t row = 0;
-  if (store) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
-  __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);
-  __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(p.v_cache);
-  float* qrot = ws_ptr<float>(p, w.qrot_off);
-  for (int j = lane; j < 64; j += 32) {
-    double s, c;
-    sincos((double)m * p.rope_freqs[j], &s, &c);
-    if (store) {
-      const int64_t ki = ((int64_t)b * p.n_kv_heads + kvh) * 128 + 2 * j;
-      const double x0 = load_in(p.k_pre, ki, p.in_dtype), x1 = load_in(p.k_pre, ki + 1, p.in_dtype);
-      __nv_bfloat162 kk;
-      kk.x = from_f64<__nv_bfloat16>(x0 * c - x1 * s);
-      kk.y = from_f64<__nv_bfloat16>(x0 * s + x1 * c);
-      reinterpret_cast<__nv_bfloat162*>(kc + row * 128)[j] = kk;
-    }
-    for (int hl = 0; hl < g; ++hl) {
-      const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
-      const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
-      reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
-    }
-  }
-  if (store)
-    for (int e = lane; e < 128; e += 32)
-      vc[row * 128 + e] =
-          from_f64<__nv_bfloat16>(load_in(p.v_in, ((int64_t)b * p.n_kv_heads + kvh) * 128 + e, p.in_dtype));
-  if (plan && lane == 0) {
-    int* lo = ws_ptr<int>(p, w.lo_off);
-    for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;
-    plan_group(p, b, kvh, m, 1);
-  }
-}
 }  // namespace
 
 template <int kRowsPerCta, int kMinBlocks>
@@ -159,24 +111,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(M
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (tid != 0) return;
   for (int w = 1; w < kThreads / 32; ++w) key = wkey[w] > key ? wkey[w] : key;
-  const Workspace ws = workspace_layout(p);
-  unsigned long long* keys = ws_ptr<unsigned long long>(p, ws.mkey_off);
-  unsigned int* arrivals = ws_ptr<unsigned int>(p, ws.marr_off);
-  if (key) atomicMax(keys + bh, key);
-  __threadfence();
-  if (atomicAdd(arrivals + bh, 1u) != (unsigned)nsplit - 1) return;
-  // last CTA of this (request, head): decide
-  __threadfence();
-  const unsigned long long k3 = atomicExch(keys + bh, 0ull);
-  arrivals[bh] = 0u;
-  double bd = CUDART_INF;
-  int bp = -1;
-  if (k3) {
-    const unsigned long long raw = ~k3;
-    bd = (double)__uint_as_float((unsigned)(raw >> 32));
-    bp = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
-  }
-  decide_head(p, bh, m, n_scan, bp > 0, bd, bp);
+  publish_and_decide(p, bh, m, n_scan, nsplit, key);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -186,15 +121,18 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-// Variants (ring rows per CTA, min CTAs per SM); MAC_FRONT_VARIANT selects one (development knob).
+cudaError_t launch_front_tc(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append, int rotate_only,
+                            int plan);
+
+// MAC_FRONT_VARIANT (development knob): 0 = persistent tensor-core front (front_tc.cu, default);
+// 1.. = this file's one-shot CUDA-core stream with (ring rows per CTA, min CTAs per SM) below.
 struct FrontVariant {
   void (*fn)(MacDecodeParams, int, int, int, int);
   int rows;
 };
 static const FrontVariant kFrontVariants[] = {
     {front_bf16_d128_kernel<128, 5>, 128}, {front_bf16_d128_kernel<64, 8>, 64},
-    {front_bf16_d128_kernel<256, 3>, 256}, {front_bf16_d128_kernel<64, 6>, 64},
-    {front_bf16_d128_kernel<128, 4>, 128}, {front_bf16_d128_kernel<32, 8>, 32},
+    {front_bf16_d128_kernel<256, 3>, 256},
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
@@ -204,9 +142,10 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   if (vi < 0) {
     const char* env = getenv("MAC_FRONT_VARIANT");
     vi = env ? atoi(env) : 0;
-    if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
+    if (vi < 0 || vi > (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
   }
-  const FrontVariant& v = kFrontVariants[vi];
+  if (vi == 0) return launch_front_tc(p, st, do_match, do_append, rotate_only, plan);
+  const FrontVariant& v = kFrontVariants[vi - 1];
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + v.rows - 1) / v.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;

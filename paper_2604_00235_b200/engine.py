@@ -82,7 +82,7 @@ class BatchDecodeEngine:
 
     def __init__(self, cfg: EngineConfig, batch: int, max_seq_len: int, *, device="cuda",
                  max_chunks: int | None = None, min_chunk: int = 128, page_perm_seed: int | None = None,
-                 record_cached: bool = False, kv_offset: int = 0):
+                 record_cached: bool = False, kv_offset: int = 0, kv_limit: int = 0, n_shards: int = 0):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         if max_seq_len < 1:
@@ -97,7 +97,11 @@ class BatchDecodeEngine:
         self.page_size = cfg.page_size
         self.max_chunks = max_chunks or default_max_chunks(batch, cfg.n_kv_heads)
         self.min_chunk = min_chunk
+        if kv_offset < 0 or kv_limit < 0 or n_shards < 0:
+            raise ValueError("kv_offset, kv_limit and n_shards must be >= 0")
         self.kv_offset = kv_offset
+        self.kv_limit = kv_limit
+        self.n_shards = n_shards
         self.record_cached = record_cached
         self._page_perm_seed = page_perm_seed
         dev = self.device
@@ -125,6 +129,11 @@ class BatchDecodeEngine:
         self.o_fallbacks = torch.zeros(B, Hq, **i32)
         self.o_cached_acc = torch.zeros(B, Hq, dv, dtype=self.sumdt, device=dev) if record_cached else None
         self.o_cached_lse = torch.zeros(B, Hq, dtype=self.sumdt, device=dev) if record_cached else None
+        # KV-sharded path (n_shards >= 1, sharded.py): this shard's (piece, band) summaries and
+        # every shard's, gathered in rank order
+        self.shard_send = torch.zeros(B, Hq, 2, dv + 1, dtype=self.sumdt, device=dev) if n_shards else None
+        self.shard_parts = (torch.zeros(n_shards, B, Hq, 2, dv + 1, dtype=self.sumdt, device=dev)
+                            if n_shards else None)
         probe = self._params(0, self.o_out, self.o_out, self.o_out, _lib.DT_F32)
         # zeroed once: the match kernel keeps its cross-CTA keys/counters zero between steps
         self.workspace = torch.zeros(int(_lib.load().mac_workspace_bytes(probe)), dtype=torch.uint8, device=dev)
@@ -189,6 +198,11 @@ class BatchDecodeEngine:
         P.in_dtype = in_dt
         P.max_chunks, P.min_chunk = self.max_chunks, self.min_chunk
         P.kv_offset = self.kv_offset
+        P.kv_limit = self.kv_limit
+        P.n_shards = self.n_shards
+        if self.shard_send is not None:
+            P.shard_out = self.shard_send.data_ptr()
+            P.shard_parts = self.shard_parts.data_ptr()
         P.thr_sq = threshold(cfg.d, cfg.tau_for(layer)) ** 2
         P.delta_max = cfg.delta_max or 0
         P.match_space = _lib.MATCH_POST_ROPE if cfg.match_space == MATCH_POST_ROPE else _lib.MATCH_PRE_ROPE
@@ -282,10 +296,12 @@ class BatchDecodeEngine:
 
     # ------------------------------------------------------------------ state injection
     def inject(self, layer: int, k_rot: torch.Tensor, v: torch.Tensor, ring_q: torch.Tensor, ring_acc: torch.Tensor,
-               ring_lse: torch.Tensor, n: int):
-        """Load a prefix state for every request: K/V rows 1..n (post-RoPE, [B, Hkv, n, d]) and the
-        ring entries of positions n-cnt+1..n ([B, Hq, cnt, ...], cnt = min(n, W), oldest first)."""
+               ring_lse: torch.Tensor, n: int, *, seq_len: int | None = None):
+        """Load a prefix state for every request: local K/V rows 1..n (post-RoPE, [B, Hkv, n, d]) and
+        the ring entries of positions L-cnt+1..L ([B, Hq, cnt, ...], cnt <= W, oldest first), where
+        L = seq_len (default n; a KV shard passes the request's global length)."""
         cfg, B, ps = self.cfg, self.batch, self.page_size
+        L = n if seq_len is None else seq_len
         self.reserve(n + 1)
         pages = -(-n // ps)
         for b in range(B):
@@ -298,12 +314,12 @@ class BatchDecodeEngine:
             self.v_cache[layer][ids] = vv.view(pages, ps, cfg.n_kv_heads, cfg.d_v).transpose(1, 2)
         cnt = ring_q.shape[2]
         W = cfg.window
-        pos = torch.arange(n - cnt + 1, n + 1, device=self.device)
+        pos = torch.arange(L - cnt + 1, L + 1, device=self.device)
         slots = (pos - 1) % W
         self.ring_q[layer][:, :, slots] = ring_q.to(self.device, self.sdt)
         self.ring_acc[layer][:, :, slots] = ring_acc.to(self.device, self.sumdt)
         self.ring_lse[layer][:, :, slots] = ring_lse.to(self.device, self.sumdt)
-        self.seq_lens[layer].fill_(n)
+        self.seq_lens[layer].fill_(L)
 
 
 # ----------------------------------------------------------------------------
