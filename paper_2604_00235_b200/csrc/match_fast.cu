@@ -121,11 +121,10 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-cudaError_t launch_front_tc(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append, int rotate_only,
-                            int plan);
-
-// MAC_FRONT_VARIANT (development knob): 0 = persistent tensor-core front (front_tc.cu, default);
-// 1.. = this file's one-shot CUDA-core stream with (ring rows per CTA, min CTAs per SM) below.
+// MAC_FRONT_VARIANT (development knob): (ring rows per CTA, min CTAs per SM) = (128,5) default,
+// (64,8), (256,3).  Measured alternatives that lost on C3 (persistent tensor-core, persistent
+// CUDA-core, f32x2 "lean", DSMEM-cluster argmin, one fused step kernel) are on branch
+// exp/fused-step; numbers in DESIGN.md §4.
 struct FrontVariant {
   void (*fn)(MacDecodeParams, int, int, int, int);
   int rows;
@@ -142,10 +141,9 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   if (vi < 0) {
     const char* env = getenv("MAC_FRONT_VARIANT");
     vi = env ? atoi(env) : 0;
-    if (vi < 0 || vi > (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
+    if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
   }
-  if (vi == 0) return launch_front_tc(p, st, do_match, do_append, rotate_only, plan);
-  const FrontVariant& v = kFrontVariants[vi - 1];
+  const FrontVariant& v = kFrontVariants[vi];
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + v.rows - 1) / v.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;

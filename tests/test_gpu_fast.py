@@ -139,3 +139,37 @@ def test_full_decode_long_context_bf16():
     for h in range(hq):
         s = orc.summarize(orc.rope_rotate(q[h], float(n + 1), freqs), kk[h // g], vv[h // g])
         assert rel_err(out[h], s.acc) <= TOL, h
+
+
+@pytest.mark.parametrize("max_chunks", [1, 3])
+def test_plan_at_list_capacity(max_chunks):
+    """Every group split into exactly max_chunks items (the work list full to capacity): the
+    amend workers' slot claims run past the list and must stop there."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
+
+    B, n, hq, hkv = 3, 3000, 8, 2
+    g = hq // hkv
+    rng = np.random.default_rng(11)
+    k = bf16_round(rng.standard_normal((B, hkv, n, 128)))
+    v = bf16_round(rng.standard_normal((B, hkv, n, 128)))
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=64, band=16, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, n + 8, max_chunks=max_chunks, min_chunk=16)
+    W = cfg.window
+    eng.inject(0, torch.from_numpy(k.astype(np.float32)).cuda(), torch.from_numpy(v.astype(np.float32)).cuda(),
+               torch.zeros(B, hq, W, 128), torch.zeros(B, hq, W, 128), torch.full((B, hq, W), -math.inf), n)
+    freqs = orc.rope_freqs(128)
+    for step in range(3):
+        m = n + step + 1
+        q = bf16_round(rng.standard_normal((B, hq, 128)))
+        kn = bf16_round(rng.standard_normal((B, hkv, 128)))
+        vn = bf16_round(rng.standard_normal((B, hkv, 128)))
+        out = eng.full_decode(0, *(torch.from_numpy(a).to("cuda", torch.bfloat16).contiguous()
+                                   for a in (q, kn, vn))).double().cpu().numpy()
+        k_rot = np.stack([[bf16_round(orc.rope_rotate(kn[b, j], float(m), freqs)) for j in range(hkv)]
+                          for b in range(B)])
+        k = np.concatenate([k, k_rot[:, :, None]], 2)
+        v = np.concatenate([v, vn[:, :, None]], 2)
+        for b in range(B):
+            for h in range(hq):
+                s = orc.summarize(orc.rope_rotate(q[b, h], float(m), freqs), k[b, h // g], v[b, h // g])
+                assert rel_err(out[b, h], s.acc) <= TOL, (step, b, h)
