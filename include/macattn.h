@@ -23,6 +23,7 @@
  *                     (no append): the per-step fidelity oracle (engine.py:507-509)
  *   mac_merge_partials  log-domain merge of per-shard (acc, lse) partials
  *                     (attention.py:119-135 merge) for the KV-sharded miss path
+ *   mac_prefill_kv    bulk KV append of a prompt (engine.py:434-437 applied to n tokens)
  *   mac_shard_partial / mac_shard_complete  decode_step split around the one
  *                     cross-GPU exchange of the KV-sharded path (all-gather of
  *                     per-shard (piece, band) summaries, then the merge)
@@ -163,6 +164,11 @@ int mac_shard_partial(const MacDecodeParams* p, void* stream);
  * cached(p) (+) pieces (+) bands in rank order, output, rho, ring write-back,
  * seq_lens advance.  Every shard computes the same result. */
 int mac_shard_complete(const MacDecodeParams* p, void* stream);
+/* prefill, bulk half: append n_tokens tokens per request at positions seq_lens+1 ..
+ * seq_lens+n_tokens (k_pre / v_in are token-major [B, n_tokens, Hkv, d]), keys RoPE'd
+ * in-kernel, then seq_lens += n_tokens.  No ring work (the reference fills rings one
+ * decode step at a time, engine.py:374-402; see BatchDecodeEngine.prefill). */
+int mac_prefill_kv(const MacDecodeParams* p, int32_t n_tokens, void* stream);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,7 @@ EXPORTS = (
     "mac_merge_partials",
     "mac_shard_partial",
     "mac_shard_complete",
+    "mac_prefill_kv",
 )
 
 
@@ -139,6 +140,8 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = C.c_int
         fn.argtypes = [C.POINTER(MacDecodeParams), C.c_void_p]
+    lib.mac_prefill_kv.restype = C.c_int
+    lib.mac_prefill_kv.argtypes = [C.POINTER(MacDecodeParams), C.c_int32, C.c_void_p]
     lib.mac_merge_partials.restype = C.c_int
     lib.mac_merge_partials.argtypes = [C.POINTER(MacMergeParams), C.c_void_p]
     if lib.mac_abi_version() != ABI_VERSION:

@@ -172,6 +172,8 @@ template <int ST, int MINB>  // cp.async stages per warp, min resident warps per
 __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, int complete_mode) {
   // programmatic dependent launch: wait for the front kernel's plan before touching it
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // and lets the complete kernel's grid launch as soon as amend warps start retiring
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 #ifdef MAC_TRACE
   unsigned long long tr_start, tr_now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));

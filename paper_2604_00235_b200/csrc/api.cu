@@ -17,6 +17,7 @@ bool amend_mma_supported(const MacDecodeParams&);
 bool match_fast_supported(const MacDecodeParams&);
 bool front_fast_supported(const MacDecodeParams&);
 cudaError_t launch_merge_partials(const MacMergeParams&, cudaStream_t);
+template <int MODE> cudaError_t launch_prefill_kv(const MacDecodeParams&, int, cudaStream_t);
 }  // namespace mac
 
 using namespace mac;
@@ -162,6 +163,19 @@ int mac_shard_complete(const MacDecodeParams* p, void* stream) {
   if (!p->shard_parts) return MAC_ERR_NULL;
   if (p->n_shards < 1) return MAC_ERR_SHAPE;
   return dispatch(p, stream, STAGE_SHARDS, true);
+}
+
+int mac_prefill_kv(const MacDecodeParams* p, int32_t n_tokens, void* stream) {
+  const int v = validate(p, false);
+  if (v) return v;
+  if (n_tokens < 0) return MAC_ERR_SHAPE;
+  if (n_tokens == 0) return MAC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (p->storage) {
+    case MAC_MODE_F32: return (int)launch_prefill_kv<MAC_MODE_F32>(*p, n_tokens, st);
+    case MAC_MODE_BF16: return (int)launch_prefill_kv<MAC_MODE_BF16>(*p, n_tokens, st);
+    default: return (int)launch_prefill_kv<MAC_MODE_F64>(*p, n_tokens, st);
+  }
 }
 
 int mac_merge_partials(const MacMergeParams* p, void* stream) {

@@ -7,6 +7,8 @@ namespace mac {
 
 template <int MODE>
 __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, int full_mode) {
+  // programmatic dependent launch: the grid is set up while the amend kernel drains
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int bh = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (bh < p.batch * p.n_q_heads) complete_head<MODE>(p, bh, full_mode);
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -15,8 +17,16 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, int fu
 
 template <int MODE>
 cudaError_t launch_complete(const MacDecodeParams& p, cudaStream_t st, int full_mode) {
-  complete_kernel<MODE><<<(p.batch * p.n_q_heads + 3) / 4, 128, 0, st>>>(p, full_mode);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((p.batch * p.n_q_heads + 3) / 4);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, complete_kernel<MODE>, p, full_mode);
 }
 
 template cudaError_t launch_complete<MAC_MODE_F32>(const MacDecodeParams&, cudaStream_t, int);

@@ -259,12 +259,46 @@ class BatchDecodeEngine:
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
-    def decode_step(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor) -> BatchStepResult:
-        """One MAC step for every request: append -> match -> amend -> complete (engine.py:410-539)."""
+    def decode_step(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor, *,
+                    force_miss: bool = False) -> BatchStepResult:
+        """One MAC step for every request: append -> match -> amend -> complete (engine.py:410-539).
+        force_miss: every head takes the miss path (exact attention), as the reference's
+        refresh gate does (engine.py:456-459)."""
         self._layer(layer)
         dt = self._check_inputs(q_pre, k_pre, v)
-        _lib.call("mac_decode_step", self._params(layer, q_pre, k_pre, v, dt), self._stream())
+        _lib.call("mac_decode_step", self._params(layer, q_pre, k_pre, v, dt, force_miss), self._stream())
         return self.result()
+
+    def prefill(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor) -> BatchStepResult | None:
+        """Append a prompt of n tokens to every request ([B, n, H, d] tensors, token-major) and
+        leave the ring exactly as n forced-miss decode steps would: the first
+        n - min(n, W) tokens go through one bulk append (mac_prefill_kv), the last min(n, W)
+        through decode steps that all take the miss path, so every ring slot holds the exact
+        prefix summary AS[1, t-r] under q_t.  Returns the last step's result."""
+        self._layer(layer)
+        cfg, B = self.cfg, self.batch
+        if q_pre.dim() != 4 or q_pre.shape[0] != B or q_pre.shape[2:] != (cfg.n_q_heads, cfg.d):
+            raise ValueError(f"expected queries [B={B}, n, {cfg.n_q_heads}, {cfg.d}], got {tuple(q_pre.shape)}")
+        n = q_pre.shape[1]
+        if tuple(k_pre.shape) != (B, n, cfg.n_kv_heads, cfg.d) or tuple(v.shape) != (B, n, cfg.n_kv_heads, cfg.d_v):
+            raise ValueError("key/value shapes do not match [B, n, Hkv, d]")
+        if n == 0:
+            return None
+        stored = int(self.seq_lens[layer].max().item()) if self.capacity else 0
+        self.reserve(stored + n + 1)
+        n_bulk = n - min(n, cfg.window)
+        if n_bulk:
+            kb, vb = k_pre[:, :n_bulk].contiguous(), v[:, :n_bulk].contiguous()
+            dt = _IN_DT[kb.dtype]
+            q0 = q_pre[:, 0].contiguous()
+            P = self._build_params(layer, q0, kb, vb, dt, False)
+            code = _lib.load().mac_prefill_kv(P, n_bulk, self._stream())
+            _lib.check(code, "mac_prefill_kv")
+        res = None
+        for t in range(n_bulk, n):
+            res = self.decode_step(layer, q_pre[:, t].contiguous(), k_pre[:, t].contiguous(), v[:, t].contiguous(),
+                                   force_miss=True)
+        return res
 
     def stage(self, name: str, layer: int, q_pre, k_pre, v, force_miss: bool = False):
         """Launch one stage (mac_append_kv | mac_match | mac_amend | mac_complete) — for profiling/tests."""

@@ -11,7 +11,8 @@ reference's metrics (acceptance = hit rate, skip ratio, kv_fraction; engine.py:
 226-243), the physical GQA KV bytes the hit path read (group spans from the
 device decisions), the match bytes, and the decode latency per
 step against this repo's full-attention decode on the same state, sampled at
-fixed positions.  The threshold sweep also varies the query noise: on the
+fixed positions (device time: each sampled step is queued behind a GPU spin so
+host launch overhead is not in it).  The threshold sweep also varies the query noise: on the
 stock preset repeat distances (~noise*sqrt(d)) sit far inside every radius,
 so tau alone is flat.
 
@@ -44,6 +45,19 @@ def _trace(args):
     return tr.q_pre[:, 0], tr.k_pre[:, 0], tr.v[:, 0]
 
 
+def _timed(fn, samples, m):
+    """Device time of one step launched behind a GPU spin, so the host's launch overhead is
+    hidden (the step's kernels run back to back)."""
+    import torch
+
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(400_000)
+    a.record()
+    fn()
+    b.record()
+    samples.append((m, a, b))
+
+
 def run_cell(traces, W, tau, batch, seq_len, sample_every, device):
     import torch
 
@@ -53,51 +67,46 @@ def run_cell(traces, W, tau, batch, seq_len, sample_every, device):
     cfg = EngineConfig(d=128, d_v=128, n_q_heads=32, n_kv_heads=8, window=W, band=256, tau=tau, storage="bf16")
     eng = BatchDecodeEngine(cfg, batch, seq_len + 1, device=device)
     r, g, hq, hkv = 256, 4, 32, 8
-    hits = torch.zeros((), dtype=torch.int64, device=device)
-    skip_frac = torch.zeros((), dtype=torch.float64, device=device)
-    grp_tok = torch.zeros((), dtype=torch.int64, device=device)
-    head_tok = torch.zeros((), dtype=torch.int64, device=device)
-    match_rows = 0
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    start.record()
+    use_log = torch.empty(seq_len, batch, hq, dtype=torch.int32, device=device)
+    pos_log = torch.empty(seq_len, batch, hq, dtype=torch.int32, device=device)
+    mac = []
     for m in range(1, seq_len + 1):
-        res = eng.decode_step(0, q_all[m - 1], k_all[m - 1], v_all[m - 1])
-        use = res.use_hit.bool()
-        pos = res.match_pos.long()
-        skipped = torch.where(use, (pos - r).clamp(min=0), torch.zeros_like(pos))   # (p - r)+ on hits
-        hits += use.sum()
-        skip_frac += (skipped.double() / m).sum()                                  # engine.py:199-201
-        head_tok += (m - skipped).sum()
-        grp_tok += (m - skipped.view(batch, hkv, g).min(-1).values).sum()        # GQA group spans
-        match_rows += batch * hq * min(m - 1, W)
-    end.record()
+        step = lambda: eng.decode_step(0, q_all[m - 1], k_all[m - 1], v_all[m - 1])  # noqa: E731
+        if m % sample_every == 0:
+            _timed(step, mac, m)
+        else:
+            step()
+        use_log[m - 1].copy_(eng.o_use)
+        pos_log[m - 1].copy_(eng.o_pos)
     torch.cuda.synchronize()
-    mac_ms = start.elapsed_time(end) / seq_len
+    # the reference's metrics (engine.py:188-243) from the logged device decisions
+    mm = torch.arange(1, seq_len + 1, device=device, dtype=torch.int64).view(-1, 1, 1)
+    use = use_log.bool()
+    skipped = torch.where(use, (pos_log.long() - r).clamp(min=0), torch.zeros_like(mm))   # (p - r)+ on hits
+    head_tok = (mm - skipped).sum()
+    grp_tok = (mm.view(-1, 1, 1) - skipped.view(seq_len, batch, hkv, g).min(-1).values).sum()  # GQA spans
     decisions = seq_len * batch * hq
     full_tok = batch * hkv * seq_len * (seq_len + 1) // 2
+    match_rows = batch * hq * sum(min(m - 1, W) for m in range(1, seq_len + 1))
     out = {
-        "window": W, "tau": tau, "acceptance": float(hits) / decisions,
-        "skip_ratio": float(skip_frac) / decisions,
+        "window": W, "tau": tau, "acceptance": float(use.sum()) / decisions,
+        "skip_ratio": float((skipped.double() / mm).sum()) / decisions,
         "kv_fraction": float(head_tok) / (hq / hkv * full_tok),
         "group_kv_fraction": float(grp_tok) / full_tok,
         "kv_bytes_read": int(grp_tok) * 2 * 128 * 2,
         "kv_bytes_full": int(full_tok) * 2 * 128 * 2,
         "match_bytes": int(match_rows) * 128 * 2,
-        "mac_ms_per_step_mean": mac_ms,
+        "mac_ms_at": {str(m): a.elapsed_time(b) for m, a, b in mac},
     }
-    # full-attention decode latency at sampled positions on a fresh engine (append + exact attention)
+    # full-attention decode on a fresh engine (append + exact attention over [1, m]), same positions
     full = BatchDecodeEngine(cfg, batch, seq_len + 1, device=device)
     samples = []
     for m in range(1, seq_len + 1):
+        step = lambda: full.full_decode(0, q_all[m - 1], k_all[m - 1], v_all[m - 1])  # noqa: E731
         if m % sample_every == 0:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            full.full_decode(0, q_all[m - 1], k_all[m - 1], v_all[m - 1])
-            b.record()
-            samples.append((m, a, b))
+            _timed(step, samples, m)
         else:
-            full.full_decode(0, q_all[m - 1], k_all[m - 1], v_all[m - 1])
+            step()
     torch.cuda.synchronize()
     out["full_ms_at"] = {str(m): a.elapsed_time(b) for m, a, b in samples}
     del eng, full

@@ -1,0 +1,88 @@
+"""GPU parity of prefill (BatchDecodeEngine.prefill: bulk mac_prefill_kv + forced-miss ring steps).
+
+A prefilled engine must hold exactly the state the reference reaches after n
+decode steps that all missed: the KV cache of positions 1..n and ring slots
+with the exact prefix summaries AS[1, t-r] under q_t.  The oracle replays the
+prompt with refresh_every = 1 (every step a forced miss, engine.py:456-459),
+then both engines decode on with the normal rule and must agree step by step.
+"""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import mac_oracle as orc  # noqa: E402
+from golden_util import bf16_round, rel_err  # noqa: E402
+
+
+@pytest.mark.parametrize("n,window,band", [(300, 64, 16), (40, 64, 16), (500, 100, 0)])
+def test_prefill_then_decode_matches_oracle(n, window, band):
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    B, hq, hkv, extra = 2, 8, 2, 40
+    L = n + extra
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=40 + s))
+           for s in range(B)]
+    q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs])  # [B, L, Hq, d]
+    k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs])
+    v = np.stack([bf16_round(t.v[:, 0]) for t in trs])
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=window, band=band, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, L + 8, page_perm_seed=5, min_chunk=32)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)  # noqa: E731
+    eng.prefill(0, dev(q[:, :n]), dev(k[:, :n]), dev(v[:, :n]))
+    assert eng.seq_lens[0].tolist() == [n] * B
+
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=window, band=band, storage="bf16")
+    oes = [orc.OracleEngine(ocfg, capacity=L + 8) for _ in range(B)]
+    forced = dataclasses.replace(ocfg, refresh_every=1)
+    for b, oe in enumerate(oes):
+        oe.cfg = forced
+        for m in range(1, n + 1):
+            oe.decode_step(0, q[b, m - 1], k[b, m - 1], v[b, m - 1], m)
+        oe.cfg = ocfg
+    # ring state: queries exact, summaries within the bf16-path tolerance
+    W = window
+    cnt = min(n, W)
+    for b, oe in enumerate(oes):
+        for pos in range(n - cnt + 1, n + 1):
+            slot = (pos - 1) % W
+            gq = eng.ring_q[0][b, :, slot].double().cpu().numpy()
+            np.testing.assert_array_equal(gq, oe.rq[0, :, slot])
+            ga = eng.ring_acc[0][b, :, slot].double().cpu().numpy()
+            gl = eng.ring_lse[0][b, :, slot].double().cpu().numpy()
+            for h in range(hq):
+                if np.isfinite(oe.rlse[0, h, slot]):
+                    assert rel_err(ga[h], oe.racc[0, h, slot]) <= 2e-4
+                    assert abs(gl[h] - oe.rlse[0, h, slot]) <= 2e-4 * max(1.0, abs(oe.rlse[0, h, slot]))
+                else:
+                    assert gl[h] == -np.inf
+    # decode on: decisions identical, outputs within tolerance
+    worst, hits = 0.0, 0
+    for m in range(n + 1, L + 1):
+        res = eng.decode_step(0, dev(q[:, m - 1]), dev(k[:, m - 1]), dev(v[:, m - 1]))
+        gh = res.match_hit.cpu().numpy().astype(bool)
+        gp = res.match_pos.cpu().numpy()
+        go = res.out.double().cpu().numpy()
+        for b, oe in enumerate(oes):
+            st = oe.decode_step(0, q[b, m - 1], k[b, m - 1], v[b, m - 1], m)
+            np.testing.assert_array_equal(gh[b], st.hit)
+            np.testing.assert_array_equal(gp[b], st.p)
+            hits += int(st.use_hit.sum())
+            for h in range(hq):
+                worst = max(worst, rel_err(go[b, h], st.outputs[h]))
+    assert hits > 0
+    assert worst <= 2e-4, worst
+
+
+def test_prefill_rejects_bad_shapes():
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
+
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=8, n_kv_heads=2, window=64, band=16, storage="bf16")
+    eng = BatchDecodeEngine(cfg, 1, 64)
+    z = torch.zeros(1, 4, 8, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        eng.prefill(0, z, z, z)  # keys must have Hkv = 2 heads
