@@ -207,7 +207,7 @@ def cpu_model():
 def run_reference_arm(args, wl):
     """--impl reference: the reference algorithm on host cores (numpy restatement, bf16 storage)."""
     cores = os.cpu_count() or 1
-    procs = max(1, min(cores, args.cpu_procs))
+    procs = max(1, min(cores, args.cpu_procs or cores, wl["batch"]))
     n0 = wl["ctx"] - args.warmup - args.steps - 1
     seeds = list(range(procs))
     r = cpu_reference(wl, n0, args.steps, args.warmup, procs, seeds)
@@ -289,7 +289,8 @@ def run_ours(args, wl):
     use_log = torch.empty(S, B, hq, dtype=torch.int32, device=dev)
     pos_log = torch.empty(S, B, hq, dtype=torch.int32, device=dev)
     m_log = torch.empty(S, B, dtype=torch.int32, device=dev)
-    outs0 = torch.empty(S, min(B, args.cpu_procs), hq, D, dtype=torch.float32, device=dev)
+    cpu_procs = max(1, min(os.cpu_count() or 1, args.cpu_procs or (os.cpu_count() or 1), B))
+    outs0 = torch.empty(S, cpu_procs, hq, D, dtype=torch.float32, device=dev)
 
     # pass 1 (the measurement): W warm-up + K timed decode steps, one engine call each
     # (3 kernels: front = append+match+plan, amend, complete), CUDA events around each
@@ -394,7 +395,7 @@ def run_ours(args, wl):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            procs = max(1, min(os.cpu_count() or 1, args.cpu_procs, B))
+            procs = cpu_procs
             cpu = cpu_reference(wl, n0, args.cpu_steps, 1, procs, seeds[:procs])
             # parity of the timed GPU steps against the CPU reference on the sampled requests
             worst = 0.0
@@ -567,7 +568,8 @@ def main():
     ap.add_argument("--page-size", type=int, default=16)
     ap.add_argument("--min-chunk", type=int, default=128)
     ap.add_argument("--full-steps", type=int, default=10)
-    ap.add_argument("--cpu-procs", type=int, default=8)
+    ap.add_argument("--cpu-procs", type=int, default=0, help="CPU reference processes (0: every host core, "
+                    "at most one per request of the workload's batch)")
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
