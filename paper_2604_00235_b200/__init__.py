@@ -39,7 +39,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # the device engines import torch; load them on first use
-    if name in ("BatchDecodeEngine", "BatchStepResult", "DecodeEngine", "run_decode", "KvStoreView",
+    if name in ("BatchDecodeEngine", "BatchStepResult", "DecodeEngine", "StepGraph", "run_decode", "KvStoreView",
                 "QueryRingView", "SummaryRingView", "TrafficCounter", "rope_freqs"):
         from . import engine
 
@@ -51,7 +51,7 @@ __all__ = [
     "AttentionSummary", "BatchDecodeEngine", "BatchStepResult", "ByteCostModel", "CancellationError",
     "DOWNDATE_REMOVE", "DOWNDATE_SPLIT", "DecodeEngine", "DecodeMetrics", "EmptySummaryError", "EngineConfig",
     "MATCH_POST_ROPE", "MATCH_PRE_ROPE", "MassExceededError", "MatchConfig", "MatchResult", "PRESETS",
-    "StepResult", "SyntheticSpec", "Trace", "TraceError", "TrafficCounter", "aux_overhead_ratio",
+    "StepGraph", "StepResult", "SyntheticSpec", "Trace", "TraceError", "TrafficCounter", "aux_overhead_ratio",
     "aux_overhead_rule_of_thumb", "break_even_gate", "compute_metrics", "empty_summary", "fidelity_efficiency",
     "finalize", "gen_synthetic", "group_kv_span", "read_trace", "run_decode", "threshold", "write_trace",
 ]

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
   // append: the step's token goes to m = seq_lens + 1; rotate_only: attend at m = seq_lens
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
   const int t_local = m - p.kv_offset;        // position inside this shard's cache
-  if (kvh == 0 && threadIdx.x == 0) mpos[b] = m;
+  if (threadIdx.x == 0) mpos[b] = m;
   const bool store_kv = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
   int64_t row = 0;
   if (store_kv) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
@@ -47,6 +47,9 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
       qrot[qi + 1] = (acc_t)(x0 * s + x1 * c);
     }
   }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_u32(ws_ptr<unsigned int>(p, workspace_layout(p).app_off) + blockIdx.x, (unsigned)m);
   if (plan && threadIdx.x == 0) {  // full-attention modes: every head reads [1, m]
     int* lo = ws_ptr<int>(p, workspace_layout(p).lo_off);
     for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;

@@ -99,12 +99,21 @@ __device__ __forceinline__ float logaddexp(float a, float b) {
 __device__ __forceinline__ float fexpm1(float x) { return expm1f(x); }
 __device__ __forceinline__ double fexpm1(double x) { return expm1(x); }
 
+
 // gpu-scope acquire-release fetch-add: orders this thread's earlier writes before
 // the increment and later reads after it (replaces a fence + atomicAdd pair)
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
@@ -185,12 +194,14 @@ struct Workspace {
   size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
   size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
   size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter, 2 amend done counter,
-                     //              3 front item counter, 4 front done counter
+                     //              5 groups planned, 7 error flag (a bounded wait gave up)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  splits planned for the group
   size_t mpos_off;   // [B] i32      position m of this step
+  size_t app_off;    // [B*Hkv] u32  position the group's append landed at (release flag)
   size_t lo_off;     // [B*Hq] i32   first token each head reads (plan)
-  size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp, c, t0, t1}
+  size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp + 1, c, t0, t1}; x = 0: empty
+                     //              slot (x is the slot's ready flag; consumers zero it)
   size_t qrot_off;   // [B*Hq*d]     rotated queries (math dtype)
   size_t part_off;   // [B*Hq*max_chunks*2*(d_v+1)] split partial summaries
   size_t total;
@@ -208,7 +219,8 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.gdone_off = align256(w.ctr_off + 64);
   w.pn_off = align256(w.gdone_off + 4 * groups);
   w.mpos_off = align256(w.pn_off + 4 * groups);
-  w.lo_off = align256(w.mpos_off + 4 * (size_t)p.batch);
+  w.app_off = align256(w.mpos_off + 4 * (size_t)p.batch);
+  w.lo_off = align256(w.app_off + 4 * groups);
   w.list_off = align256(w.lo_off + 4 * rows);
   w.qrot_off = align256(w.list_off + 16 * groups * p.max_chunks);
   w.part_off = align256(w.qrot_off + acc * rows * p.head_dim);
@@ -238,8 +250,13 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
     if (base + c >= cap) break;  // cannot happen when every step is completed
     const int t0 = start + c * ch.len;
     const int t1 = min(end, t0 + ch.len - 1);
-    list[base + c] = make_int4(grp, c, t0, t1);
+    int4* e = list + base + c;
+    e->y = c;
+    e->z = t0;
+    e->w = t1;
+    st_release_u32(reinterpret_cast<unsigned*>(&e->x), (unsigned)(grp + 1));  // publish
   }
+  atom_add_acq_rel(ctr + 5, 1u);  // groups planned: the list is final once this reaches B*Hkv
 }
 
 // Decide one (request, q head) from its best candidate, apply the gates, write

@@ -356,6 +356,49 @@ class BatchDecodeEngine:
         self.seq_lens[layer].fill_(L)
 
 
+class StepGraph:
+    """One decode step of a BatchDecodeEngine layer as a replayable CUDA graph, with the
+    step's host I/O inside it: pinned host inputs -> device, the step's kernels, output ->
+    pinned host.  The serving loop writes a step's q/k/v into `q_host`/`k_host`/`v_host`,
+    calls `replay()`, and reads `out_host` after the stream syncs.  Replays are
+    stream-ordered and advance the engine like `decode_step` (every kernel reads its
+    position from `seq_lens`, every workspace counter returns to zero by the end of the
+    step), so one graph serves every step of the layer."""
+
+    def __init__(self, eng: "BatchDecodeEngine", layer: int, dtype=torch.bfloat16):
+        cfg, B = eng.cfg, eng.batch
+        eng._layer(layer)
+        self.eng, self.layer = eng, layer
+        dev = eng.device
+        # q, k and v share one pinned staging buffer and one device buffer: one H2D copy per step
+        nq, nk, nv = B * cfg.n_q_heads * cfg.d, B * cfg.n_kv_heads * cfg.d, B * cfg.n_kv_heads * cfg.d_v
+        self.in_host = torch.zeros(nq + nk + nv, dtype=dtype).pin_memory()
+        self.in_dev = torch.zeros(nq + nk + nv, dtype=dtype, device=dev)
+        split = lambda t: (t[:nq].view(B, cfg.n_q_heads, cfg.d), t[nq:nq + nk].view(B, cfg.n_kv_heads, cfg.d),  # noqa: E731
+                           t[nq + nk:].view(B, cfg.n_kv_heads, cfg.d_v))
+        self.q_host, self.k_host, self.v_host = split(self.in_host)
+        self.q_dev, self.k_dev, self.v_dev = split(self.in_dev)
+        self.out_host = torch.zeros(B, cfg.n_q_heads, cfg.d_v, dtype=eng.sumdt).pin_memory()
+        self.graph = torch.cuda.CUDAGraph()
+        self.h2d_bytes = self.in_host.numel() * self.in_host.element_size()
+        self.d2h_bytes = self.out_host.numel() * self.out_host.element_size()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        # thread-local capture: the launchers' one-time setup (function attributes, occupancy
+        # queries) is not a stream operation and may run during the first capture
+        with torch.cuda.graph(self.graph, stream=s, capture_error_mode="thread_local"):
+            self._body()
+
+    def _body(self):
+        eng = self.eng
+        self.in_dev.copy_(self.in_host, non_blocking=True)
+        eng.decode_step(self.layer, self.q_dev, self.k_dev, self.v_dev)
+        self.out_host.copy_(eng.o_out, non_blocking=True)
+
+    def replay(self):
+        self.graph.replay()
+
+
 # ----------------------------------------------------------------------------
 # reference-shaped single-request shim
 # ----------------------------------------------------------------------------

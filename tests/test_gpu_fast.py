@@ -173,3 +173,34 @@ def test_plan_at_list_capacity(max_chunks):
             for h in range(hq):
                 s = orc.summarize(orc.rope_rotate(q[b, h], float(m), freqs), k[b, h // g], v[b, h // g])
                 assert rel_err(out[b, h], s.acc) <= TOL, (step, b, h)
+
+
+def test_step_graph_replay_equals_decode_step():
+    """StepGraph (H2D inputs + step kernels + D2H output captured once, replayed per step)
+    advances the engine exactly like decode_step: identical outputs, decisions and rings."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, StepGraph, SyntheticSpec, gen_synthetic
+
+    L, B, hq, hkv = 200, 2, 8, 2
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=70 + s))
+           for s in range(B)]
+    q = torch.from_numpy(np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)).bfloat16()  # [L, B, H, d]
+    k = torch.from_numpy(np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)).bfloat16()
+    v = torch.from_numpy(np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)).bfloat16()
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=64, band=16, storage="bf16")
+    direct = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    graphed = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    sg = StepGraph(graphed, 0)
+    hits = 0
+    for m in range(1, L + 1):
+        res = direct.decode_step(0, q[m - 1].cuda(), k[m - 1].cuda(), v[m - 1].cuda())
+        sg.q_host.copy_(q[m - 1])
+        sg.k_host.copy_(k[m - 1])
+        sg.v_host.copy_(v[m - 1])
+        sg.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(sg.out_host, res.out.cpu()), m
+        assert torch.equal(graphed.o_pos, direct.o_pos)
+        hits += int(direct.o_use.sum())
+    assert hits > 0
+    assert torch.equal(graphed.ring_acc[0], direct.ring_acc[0]) and torch.equal(graphed.ring_q[0], direct.ring_q[0])
+    assert graphed.seq_lens[0].tolist() == [L] * B
