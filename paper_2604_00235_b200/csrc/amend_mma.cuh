@@ -64,6 +64,14 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// the same MMA with a zero accumulator (no register zeroing before the first k-step)
+__device__ __forceinline__ void mma16816_z(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};\n"
+      : "=f"(c[0]), "=f"(c[1]), "=f"(c[2]), "=f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);  // .x = lo_elem (low 16 bits)
   return *reinterpret_cast<uint32_t*>(&v);
@@ -196,6 +204,14 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
   };
   long long rows_cur = rows_of(0), rows_nxt = nsub > 32 ? rows_of(1) : 0;
   int blk_cur = 0;
+  // this lane's 16-byte chunk of each of the 8 copy rounds: tile row 2*rr + (lane >> 4),
+  // column lane & 15; the XOR swizzle repeats every 4 rounds (rows 8 apart), so four
+  // offsets cover all eight (+2048 bytes for rounds 4-7), global offsets are linear
+  const int chi = lane >> 4, ccol = lane & 15;
+  uint32_t soff[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) soff[i] = swz(2 * i + chi, ccol);
+  const int goff = chi * 256 + ccol * 16;
   auto issue = [&](int j, int stage) {
     if ((j >> 5) != blk_cur) {
       blk_cur = j >> 5;
@@ -208,9 +224,9 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
     const uint32_t ks_ = sm + stage * 2 * TILE_BYTES, vs_ = ks_ + TILE_BYTES;
 #pragma unroll
     for (int rr = 0; rr < 8; ++rr) {
-      const int ci = lane + 32 * rr, trow = ci >> 4, col = ci & 15;
-      cp_async16(ks_ + swz(trow, col), kg + trow * 256 + col * 16);
-      cp_async16(vs_ + swz(trow, col), vg + trow * 256 + col * 16);
+      const uint32_t so = soff[rr & 3] + (rr >= 4 ? 2048u : 0u);
+      cp_async16(ks_ + so, kg + goff + rr * 512);
+      cp_async16(vs_ + so, vg + goff + rr * 512);
     }
   };
   // KV streams first; the query fragments and head bounds load underneath
@@ -261,11 +277,7 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
     const uint32_t ks0 = sm + (j0 % ST) * 2 * TILE_BYTES, vs0 = ks0 + TILE_BYTES;
     const uint32_t ks1 = sm + ((j0 + 1) % ST) * 2 * TILE_BYTES, vs1 = ks1 + TILE_BYTES;
     // S = Q K^T for 4 n-tiles (32 tokens); even/odd k-steps accumulate separately
-    float s[4][2][4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) s[nt][h2][0] = s[nt][h2][1] = s[nt][h2][2] = s[nt][h2][3] = 0.f;
+    float s[4][2][4];  // k-steps 0 and 1 start the two chains with a zero accumulator
     {
       const int mi = lane >> 3, ii = lane & 7;
       const int trow = ((mi >> 1) << 3) + ii;
@@ -273,13 +285,23 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
       for (int ks = 0; ks < 8; ++ks) {
         uint32_t b0, b1, b2, b3;
         ldsm_x4(ks0 + swz(trow, 2 * ks + (mi & 1)), b0, b1, b2, b3);
-        mma16816(s[0][ks & 1], qa[ks], b0, b1);
-        mma16816(s[1][ks & 1], qa[ks], b2, b3);
+        if (ks < 2) {
+          mma16816_z(s[0][ks & 1], qa[ks], b0, b1);
+          mma16816_z(s[1][ks & 1], qa[ks], b2, b3);
+        } else {
+          mma16816(s[0][ks & 1], qa[ks], b0, b1);
+          mma16816(s[1][ks & 1], qa[ks], b2, b3);
+        }
         if (has1) {
           uint32_t c0, c1, c2, c3;
           ldsm_x4(ks1 + swz(trow, 2 * ks + (mi & 1)), c0, c1, c2, c3);
-          mma16816(s[2][ks & 1], qa[ks], c0, c1);
-          mma16816(s[3][ks & 1], qa[ks], c2, c3);
+          if (ks < 2) {
+            mma16816_z(s[2][ks & 1], qa[ks], c0, c1);
+            mma16816_z(s[3][ks & 1], qa[ks], c2, c3);
+          } else {
+            mma16816(s[2][ks & 1], qa[ks], c0, c1);
+            mma16816(s[3][ks & 1], qa[ks], c2, c3);
+          }
         }
       }
     }
