@@ -275,7 +275,8 @@ def run_ours(args, wl):
     W_, K = args.warmup, args.steps
     cfg = EngineConfig(d=D, d_v=D, n_q_heads=hq, n_kv_heads=hkv, window=WINDOW, band=BAND, tau=TAU, storage="bf16",
                        page_size=args.page_size)
-    eng = BatchDecodeEngine(cfg, B, wl["ctx"] + args.full_steps + 64, device=dev, min_chunk=args.min_chunk)
+    eng = BatchDecodeEngine(cfg, B, wl["ctx"] + args.full_steps + 64, device=dev, min_chunk=args.min_chunk,
+                            max_chunks=args.max_chunks or None)
     inject_into_engine(eng, 0, states, n0, bulk_seed=rank)
     bf = torch.bfloat16
     q_all = torch.from_numpy(np.stack([s.step_q for s in states], 1)).to(dev, bf)  # [S, B, Hq, d]
@@ -493,7 +494,8 @@ def run_c4(args, wl):
                        page_size=args.page_size)
     T = tail_len(WINDOW, BAND)
     layout = ShardLayout.for_context(ctx, world, min_tail=T + S + 1)
-    eng = ShardedDecodeEngine(cfg, 1, layout, rank, ctx + 8, device=dev, min_chunk=args.min_chunk)
+    eng = ShardedDecodeEngine(cfg, 1, layout, rank, ctx + 8, device=dev, min_chunk=args.min_chunk,
+                              max_chunks=args.max_chunks or None)
     e = eng.engine
     lo, hi = layout.local_range(rank, n0)
     n_local = hi - lo + 1
@@ -576,6 +578,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--page-size", type=int, default=16)
     ap.add_argument("--min-chunk", type=int, default=128)
+    ap.add_argument("--max-chunks", type=int, default=0, help="split-KV slots per group (0: engine default)")
     ap.add_argument("--full-steps", type=int, default=10)
     ap.add_argument("--cpu-procs", type=int, default=0, help="CPU reference processes (0: every host core, "
                     "at most one per request of the workload's batch)")

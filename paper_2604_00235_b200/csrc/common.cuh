@@ -246,16 +246,17 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
   const int grp = b * p.n_kv_heads + kvh;
   ws_ptr<int>(p, w.pn_off)[grp] = ch.n;
   const unsigned base = atomicAdd(ctr, (unsigned)ch.n);
-  for (int c = 0; c < ch.n; ++c) {
-    if (base + c >= cap) break;  // cannot happen when every step is completed
+  const int n = (int)min((unsigned)ch.n, base < cap ? cap - base : 0u);  // full list: cannot happen
+  for (int c = 0; c < n; ++c) {
     const int t0 = start + c * ch.len;
-    const int t1 = min(end, t0 + ch.len - 1);
     int4* e = list + base + c;
     e->y = c;
     e->z = t0;
-    e->w = t1;
-    st_release_u32(reinterpret_cast<unsigned*>(&e->x), (unsigned)(grp + 1));  // publish
+    e->w = min(end, t0 + ch.len - 1);
   }
+  // publish: one fence, then the x words (grp + 1), each slot's ready flag
+  __threadfence();
+  for (int c = 0; c < n; ++c) list[base + c].x = grp + 1;
   atom_add_acq_rel(ctr + 5, 1u);  // groups planned: the list is final once this reaches B*Hkv
 }
 
