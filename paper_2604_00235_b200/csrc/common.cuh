@@ -204,6 +204,7 @@ struct Workspace {
                      //              slot (x is the slot's ready flag; consumers zero it)
   size_t qrot_off;   // [B*Hq*d]     rotated queries (math dtype)
   size_t part_off;   // [B*Hq*max_chunks*2*(d_v+1)] split partial summaries
+  size_t hpart_off;  // [B*Hq*W] f32  two-pass match: distance over the first d/2 dims per ring row
   size_t total;
 };
 __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -224,7 +225,8 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.list_off = align256(w.lo_off + 4 * rows);
   w.qrot_off = align256(w.list_off + 16 * groups * p.max_chunks);
   w.part_off = align256(w.qrot_off + acc * rows * p.head_dim);
-  w.total = align256(w.part_off + acc * rows * p.max_chunks * 2 * (p.head_dim_v + 1));
+  w.hpart_off = align256(w.part_off + acc * rows * p.max_chunks * 2 * (p.head_dim_v + 1));
+  w.total = align256(w.hpart_off + 4 * rows * (size_t)p.window);
   return w;
 }
 

@@ -47,7 +47,7 @@ __device__ __forceinline__ float dist8(const float* q, uint4 c) {
 template <int kRowsPerCta, int kMinBlocks>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(MacDecodeParams p, int n_match,
                                                                                int do_append, int rotate_only,
-                                                                               int plan) {
+                                                                               int plan, int /*unused*/) {
   constexpr int kLoads = kRowsPerCta / 16;  // per thread: 8 warps x 2 rows per load instruction
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the first n_append CTAs append (one warp per (request, kv head)); they are
@@ -114,6 +114,199 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(M
   publish_and_decide(p, bh, m, n_scan, nsplit, key);
 }
 
+// ---------------------------------------------------------------------------
+// Two-pass match (default for the bf16 d=128 decode step).
+//
+// Pass 1 (front_half_kernel) reads only the first d/2 = 64 dims of every ring
+// row (128 of its 256 bytes; 32-byte sectors, so the other half is never
+// fetched) and stores the partial distance P(r) = sum_{k<64} (q_k - c_k)^2 of
+// every row: a pure stream, no cross-CTA reduction, no atomics.
+// Pass 2 (verify_kernel, one CTA per (request, head), programmatic dependent
+// launch) takes the row with the smallest P, completes its distance with its
+// second half into a bound D* >= min_r D(r), keeps the rows with P(r) <= D*
+// — every other row has D(r) = P(r) + S(r) >= P(r) > D* >= min D, with S(r) >= 0
+// a sum of squares, so it can neither be the argmin nor tie it — completes
+// their distances, takes the exact argmin (ties -> larger position,
+// matching.py:171-173) and decides the head (decide_head).  On the hit path
+// the survivors are the few near-repeats, so the match reads about half the
+// ring bytes; when nearly every row survives (a fresh query, all distances
+// ~2d) pass 2 reads the second halves of all rows — the one-pass bytes.  The
+// distance is the one-pass kernel's fp32 sum of squares split in two sums.
+__global__ void __launch_bounds__(kThreads, 5) front_half_kernel(MacDecodeParams p, int n_match, int do_append,
+                                                                 int rotate_only, int plan, int /*unused*/) {
+  constexpr int kRowsPerCta = 128, kLoads = kRowsPerCta / 32;  // 8 lanes per row, 4 rows per warp-load
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if ((int)blockIdx.x < n_append) {
+    const int i = blockIdx.x * (kThreads / 32) + warp;
+    if (i < p.batch * p.n_kv_heads) append_warp(p, i, rotate_only, plan);
+    return;
+  }
+  const int W = p.window;
+  const int nsplit = (W + kRowsPerCta - 1) / kRowsPerCta;
+  const int bh = (blockIdx.x - n_append) / nsplit, split = (blockIdx.x - n_append) % nsplit;
+  const int b = bh / p.n_q_heads;
+  const int m = p.seq_lens[b] + 1;
+  const int sub = lane & 7, quad = lane >> 3;
+  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
+  const int row0 = split * kRowsPerCta;
+  uint4 v[kLoads];
+#pragma unroll
+  for (int k = 0; k < kLoads; ++k) {
+    const int slot = row0 + k * 32 + warp * 4 + quad;
+    v[k] = slot < W ? ld_stream(ring + (int64_t)slot * 16 + sub) : make_uint4(0, 0, 0, 0);
+  }
+  float q[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + sub * 8 + i, p.in_dtype);
+  int first = m - W;
+  if (first < 1) first = 1;
+  if (p.delta_max > 0 && m - p.delta_max > first) first = m - p.delta_max;
+  const int last = m - 1;
+  const int cur_slot = last >= 1 ? (last - 1) % W : 0;
+  float* hpart = ws_ptr<float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
+#pragma unroll
+  for (int k = 0; k < kLoads; ++k) {
+    const int slot = row0 + k * 32 + warp * 4 + quad;
+    float d = dist8(q, v[k]);
+    d += __shfl_xor_sync(0xffffffffu, d, 4);
+    d += __shfl_xor_sync(0xffffffffu, d, 2);
+    d += __shfl_xor_sync(0xffffffffu, d, 1);
+    const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
+    const bool live = slot < W && last >= 1 && pos >= first;
+    if (sub == 0 && slot < W) hpart[slot] = live ? d : CUDART_INF_F;  // dead rows: +inf, never survive
+  }
+}
+
+// Pass 2: one CTA per (request, head).
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = p.window;
+  const int b = bh / p.n_q_heads;
+  const int m = p.seq_lens[b] + 1;
+  const float* hpart = ws_ptr<const float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
+  int first = m - W;
+  if (first < 1) first = 1;
+  if (p.delta_max > 0 && m - p.delta_max > first) first = m - p.delta_max;
+  const int last = m - 1;
+  const int n_scan = last >= first ? last - first + 1 : 0;
+  const int cur_slot = last >= 1 ? (last - 1) % W : 0;
+  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
+  const int sub = lane & 7, quad = lane >> 3;
+  float qh[8];  // second-half query dims of this lane
+#pragma unroll
+  for (int i = 0; i < 8; ++i) qh[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + 64 + sub * 8 + i, p.in_dtype);
+  __shared__ int surv[1024];
+  __shared__ int n_surv;
+  __shared__ float sbest[8];
+  __shared__ int sslot[8];
+  __shared__ float s_dstar;
+  __shared__ unsigned long long wkey[8];
+  // (1) the smallest partial and its row
+  float bp = CUDART_INF_F;
+  int bs = -1;
+  for (int slot = tid; slot < W; slot += 256) {
+    const float pr = __ldcg(hpart + slot);
+    if (pr < bp) { bp = pr; bs = slot; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, bp, o);
+    const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+    if (ob < bp) { bp = ob; bs = os; }
+  }
+  if (lane == 0) { sbest[warp] = bp; sslot[warp] = bs; }
+  if (tid == 0) n_surv = 0;
+  __syncthreads();
+  // (2) warp 0 completes that row's distance: the bound D*
+  if (warp == 0) {
+    bp = lane < 8 ? sbest[lane] : CUDART_INF_F;
+    bs = lane < 8 ? sslot[lane] : -1;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+      if (ob < bp) { bp = ob; bs = os; }
+    }
+    bp = __shfl_sync(0xffffffffu, bp, 0);
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    float d2 = 0.f;
+    if (bs >= 0 && lane < 8) d2 = dist8(qh, ld_stream(ring + (int64_t)bs * 16 + 8 + lane));
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+    if (lane == 0) s_dstar = bs >= 0 ? bp + d2 : CUDART_INF_F;
+  }
+  __syncthreads();
+  const float D = s_dstar;
+  // (3) survivors: P(r) <= D* (dead rows hold +inf)
+  for (int slot = tid; slot < W; slot += 256) {
+    const float pr = __ldcg(hpart + slot);
+    if (pr <= D && pr != CUDART_INF_F) {
+      const int i = atomicAdd(&n_surv, 1);
+      if (i < 1024) surv[i] = slot;
+    }
+  }
+  __syncthreads();
+  const int ns = n_surv;
+  const int limit = ns <= 1024 ? ns : W;  // more survivors than the list holds (W > 1024): every row
+  // (4) their second halves: 8 lanes per row, 4 rows per warp per round
+  unsigned long long key = 0ull;
+  for (int base = warp * 4; base < limit; base += 32) {
+    const int idx = base + quad;
+    int slot = -1;
+    if (idx < limit) slot = ns <= 1024 ? surv[idx] : idx;
+    float d2 = 0.f;
+    if (slot >= 0) d2 = dist8(qh, ld_stream(ring + (int64_t)slot * 16 + 8 + sub));
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+    if (slot >= 0 && sub == 0) {
+      const float pr = __ldcg(hpart + slot);
+      if (pr != CUDART_INF_F) {
+        const float d = pr + d2;
+        const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
+        const unsigned long long k2 =
+            ~(((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos));
+        key = k2 > key ? k2 : key;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+    key = other > key ? other : key;
+  }
+  if (lane == 0) wkey[warp] = key;
+  __syncthreads();
+  if (tid != 0) return;
+  for (int w = 1; w < 8; ++w) key = wkey[w] > key ? wkey[w] : key;
+  double bd = CUDART_INF;
+  int bpos = -1;
+  if (key) {
+    const unsigned long long raw = ~key;
+    bd = (double)__uint_as_float((unsigned)(raw >> 32));
+    bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
+  }
+  decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos);
+}
+
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.batch * p.n_q_heads);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, verify_kernel, p);
+}
+
 bool match_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128 && p.match_space == MAC_MATCH_PRE_ROPE;
 }
@@ -121,17 +314,20 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-// MAC_FRONT_VARIANT (development knob): (ring rows per CTA, min CTAs per SM) = (128,5) default,
-// (64,8), (256,3).  Measured alternatives that lost on C3 (persistent tensor-core, persistent
+// MAC_FRONT_VARIANT (development knob): 0 = two-pass match (default), 1-3 = one-pass stream with
+// (ring rows per CTA, min CTAs per SM) = (128,5), (64,8), (256,3).  Measured alternatives that lost on C3 (persistent tensor-core, persistent
 // CUDA-core, f32x2 "lean", DSMEM-cluster argmin, one fused step kernel) are on branch
 // exp/fused-step; numbers in DESIGN.md §4.
 struct FrontVariant {
-  void (*fn)(MacDecodeParams, int, int, int, int);
+  void (*fn)(MacDecodeParams, int, int, int, int, int);
   int rows;
+  bool two_pass;  // front_half_kernel + verify_kernel
 };
 static const FrontVariant kFrontVariants[] = {
-    {front_bf16_d128_kernel<128, 5>, 128}, {front_bf16_d128_kernel<64, 8>, 64},
-    {front_bf16_d128_kernel<256, 3>, 256},
+    {front_half_kernel, 128, true},
+    {front_bf16_d128_kernel<128, 5>, 128, false},
+    {front_bf16_d128_kernel<64, 8>, 64, false},
+    {front_bf16_d128_kernel<256, 3>, 256, false},
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
@@ -147,8 +343,12 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + v.rows - 1) / v.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;
-  v.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan);
-  return cudaGetLastError();
+  // the two-pass front covers the match stage only: append-only launches use the one-pass kernel
+  const FrontVariant& u = (v.two_pass && !do_match) ? kFrontVariants[1] : v;
+  u.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
+  cudaError_t e = cudaGetLastError();
+  if (e || !(u.two_pass && do_match)) return e;
+  return launch_verify(p, st);
 }
 
 }  // namespace mac
