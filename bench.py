@@ -113,16 +113,23 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # algorithmic bytes
 # ----------------------------------------------------------------------------
-def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2):
+def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass=True):
     """Per-request algorithmic bytes of one MAC step, from the step's device decisions.
 
-    use/pos: [B, Hq] arrays; m: [B] positions.  Returns dict of totals over the batch."""
+    use/pos: [B, Hq] arrays; m: [B] positions.  Returns dict of totals over the batch.
+    Two-pass match (default): the first d/2 dims of every live ring row, a 4-byte partial
+    written and read back per row, and the query; the second halves of the few rows that
+    survive the bound are not counted (a lower bound: the GB/s derived from it cannot be
+    overstated; ncu's DRAM bytes cross-check it in profiles/)."""
     g = hq // hkv
     B = use.shape[0]
     match = kv = summ = 0
     for b in range(B):
         live = min(int(m[b]) - 1, window)
-        match += hq * live * d * s_ring + hq * d * s_ring
+        if two_pass:
+            match += hq * live * (d // 2) * s_ring + hq * window * 4 * 2 + hq * d * s_ring
+        else:
+            match += hq * live * d * s_ring + hq * d * s_ring
         for j in range(hkv):
             u = use[b, j * g:(j + 1) * g]
             p = pos[b, j * g:(j + 1) * g]
@@ -338,7 +345,8 @@ def run_ours(args, wl):
     use = use_log.cpu().numpy()
     pos = pos_log.cpu().numpy()
     mm = m_log.cpu().numpy()
-    byts = [step_bytes(use[s], pos[s], mm[s], hq, hkv, D, WINDOW, BAND) for s in range(W_, S)]
+    two_pass = os.environ.get("MAC_FRONT_VARIANT", "0") == "0"
+    byts = [step_bytes(use[s], pos[s], mm[s], hq, hkv, D, WINDOW, BAND, two_pass=two_pass) for s in range(W_, S)]
     hit_rate = float(use[W_:].mean())
 
     # full-attention decode baseline on the same state (runs after the MAC steps: it does not write rings)

@@ -262,12 +262,12 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
   atom_add_acq_rel(ctr + 5, 1u);  // groups planned: the list is final once this reaches B*Hkv
 }
 
-// Decide one (request, q head) from its best candidate, apply the gates, write
-// the match outputs and the head's first token; the last head of a GQA group
-// to be decided plans the group (matching.py:171-175; engine.py:449-459).
-__device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
-                                            double bdist, int bpos) {
-  const int W = p.window, Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv;
+// Decide one (request, q head) from its best candidate and apply the gates;
+// writes the match outputs and returns the first token the head reads
+// (matching.py:171-175; engine.py:449-459).
+__device__ __forceinline__ int decide_one(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
+                                          double bdist, int bpos) {
+  const int W = p.window;
   const bool hit = n_scan > 0 && have && bdist < p.thr_sq;
   const int pp = hit ? bpos : -1;
   bool use = hit;
@@ -280,9 +280,18 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
   p.match_dist[bh] = n_scan > 0 ? bdist : CUDART_INF;
   p.match_scanned[bh] = n_scan;
   p.use_hit[bh] = use;
+  const int lo = head_lo(use, pp, p.band);
+  ws_ptr<int>(p, workspace_layout(p).lo_off)[bh] = lo;
+  return lo;
+}
+
+// decide_one, and the last head of a GQA group to be decided plans the group
+__device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
+                                            double bdist, int bpos) {
+  const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv;
+  decide_one(p, bh, m, n_scan, have, bdist, bpos);
   const Workspace w = workspace_layout(p);
-  int* lo = ws_ptr<int>(p, w.lo_off);
-  lo[bh] = head_lo(use, pp, p.band);
+  const int* lo = ws_ptr<const int>(p, w.lo_off);
   const int b = bh / Hq, h = bh % Hq, kvh = h / g;
   unsigned int* gcnt = ws_ptr<unsigned int>(p, w.gcnt_off);
   const unsigned prev = atom_add_acq_rel(gcnt + b * Hkv + kvh, 1u);

@@ -179,124 +179,155 @@ __global__ void __launch_bounds__(kThreads, 5) front_half_kernel(MacDecodeParams
   }
 }
 
-// Pass 2: one CTA per (request, head).
+// Pass 2: one CTA per GQA group (request, kv head), 8 warps: 8/g warps per head,
+// each owning a contiguous share of the head's ring rows.
+//   1. every warp takes the two smallest partials of its share as candidates and
+//      completes their distances (their second halves, one load round);
+//   2. the head's bound D* = the smallest candidate distance (shared memory);
+//   3. every warp completes the distances of the other rows of its share with
+//      P(r) <= D* (usually none on the hit path);
+//   4. per head: exact argmin over candidates and survivors, decide_one; the
+//      group is planned in the same CTA (no cross-CTA arrival).
 __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int W = p.window;
-  const int b = bh / p.n_q_heads;
+  const int grp = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
+  const int wph = 8 / g;                          // warps per head
+  const int hl = warp / wph, part = warp % wph;   // head in the group, share of its rows
+  const bool active = hl < g;
+  const int b = grp / Hkv, kvh = grp % Hkv;
+  const int bh = b * Hq + kvh * g + (active ? hl : 0);
   const int m = p.seq_lens[b] + 1;
-  const float* hpart = ws_ptr<const float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
   int first = m - W;
   if (first < 1) first = 1;
   if (p.delta_max > 0 && m - p.delta_max > first) first = m - p.delta_max;
   const int last = m - 1;
   const int n_scan = last >= first ? last - first + 1 : 0;
   const int cur_slot = last >= 1 ? (last - 1) % W : 0;
+  const int share = (W + wph - 1) / wph;
+  const int r0 = part * share, r1 = min(W, r0 + share);
+  const float* hpart = ws_ptr<const float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
   const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
   const int sub = lane & 7, quad = lane >> 3;
-  float qh[8];  // second-half query dims of this lane
+  float qh[8];  // second-half query dims of this lane's 8-lane row group
 #pragma unroll
   for (int i = 0; i < 8; ++i) qh[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + 64 + sub * 8 + i, p.in_dtype);
-  __shared__ int surv[1024];
-  __shared__ int n_surv;
-  __shared__ float sbest[8];
-  __shared__ int sslot[8];
-  __shared__ float s_dstar;
-  __shared__ unsigned long long wkey[8];
-  // (1) the smallest partial and its row
-  float bp = CUDART_INF_F;
-  int bs = -1;
-  for (int slot = tid; slot < W; slot += 256) {
-    const float pr = __ldcg(hpart + slot);
-    if (pr < bp) { bp = pr; bs = slot; }
-  }
+  auto pos_of = [&](int slot) { return last - cur_slot + slot - (slot > cur_slot ? W : 0); };
+  auto key_of = [&](float d, int slot) {
+    return ~(((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos_of(slot)));
+  };
+  // 1. two smallest partials of this warp's share
+  float p1 = CUDART_INF_F, p2 = CUDART_INF_F;
+  int s1 = -1, s2 = -1;
+  if (active)
+    for (int slot = r0 + lane; slot < r1; slot += 32) {
+      const float pr = __ldcg(hpart + slot);
+      if (pr < p1) { p2 = p1; s2 = s1; p1 = pr; s1 = slot; }
+      else if (pr < p2) { p2 = pr; s2 = slot; }
+    }
+  float c1 = p1;
+  int cs1 = s1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, bp, o);
-    const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-    if (ob < bp) { bp = ob; bs = os; }
+    const float ob = __shfl_xor_sync(0xffffffffu, c1, o);
+    const int os = __shfl_xor_sync(0xffffffffu, cs1, o);
+    if (ob < c1 || (ob == c1 && os > cs1)) { c1 = ob; cs1 = os; }
   }
-  if (lane == 0) { sbest[warp] = bp; sslot[warp] = bs; }
-  if (tid == 0) n_surv = 0;
-  __syncthreads();
-  // (2) warp 0 completes that row's distance: the bound D*
-  if (warp == 0) {
-    bp = lane < 8 ? sbest[lane] : CUDART_INF_F;
-    bs = lane < 8 ? sslot[lane] : -1;
+  float c2 = (s1 == cs1) ? p2 : p1;  // the lane that gave the minimum offers its runner-up
+  int cs2 = (s1 == cs1) ? s2 : s1;
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      const float ob = __shfl_xor_sync(0xffffffffu, bp, o);
-      const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-      if (ob < bp) { bp = ob; bs = os; }
-    }
-    bp = __shfl_sync(0xffffffffu, bp, 0);
-    bs = __shfl_sync(0xffffffffu, bs, 0);
-    float d2 = 0.f;
-    if (bs >= 0 && lane < 8) d2 = dist8(qh, ld_stream(ring + (int64_t)bs * 16 + 8 + lane));
-    d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
-    d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
-    d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
-    if (lane == 0) s_dstar = bs >= 0 ? bp + d2 : CUDART_INF_F;
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, c2, o);
+    const int os = __shfl_xor_sync(0xffffffffu, cs2, o);
+    if (ob < c2 || (ob == c2 && os > cs2)) { c2 = ob; cs2 = os; }
   }
+  // their full distances: lanes 0-7 candidate 1, lanes 8-15 candidate 2
+  const int cslot = quad == 0 ? cs1 : (quad == 1 ? cs2 : -1);
+  const float cpart = quad == 0 ? c1 : c2;
+  float d2 = 0.f;
+  if (cslot >= 0 && cpart != CUDART_INF_F) d2 = dist8(qh, ld_stream(ring + (int64_t)cslot * 16 + 8 + sub));
+  d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
+  d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
+  d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+  const bool cvalid = cslot >= 0 && cpart != CUDART_INF_F;
+  const float cfull = cvalid ? cpart + d2 : CUDART_INF_F;
+  unsigned long long key = (cvalid && sub == 0 && quad < 2) ? key_of(cfull, cslot) : 0ull;
+  float dmin = fminf(__shfl_sync(0xffffffffu, cfull, 0), __shfl_sync(0xffffffffu, cfull, 8));
+  // 2. the head's bound
+  __shared__ float sD[8];
+  __shared__ unsigned long long skey[8];
+  __shared__ int slo[8];
+  if (lane == 0) sD[warp] = dmin;
   __syncthreads();
-  const float D = s_dstar;
-  // (3) survivors: P(r) <= D* (dead rows hold +inf)
-  for (int slot = tid; slot < W; slot += 256) {
-    const float pr = __ldcg(hpart + slot);
-    if (pr <= D && pr != CUDART_INF_F) {
-      const int i = atomicAdd(&n_surv, 1);
-      if (i < 1024) surv[i] = slot;
-    }
-  }
-  __syncthreads();
-  const int ns = n_surv;
-  const int limit = ns <= 1024 ? ns : W;  // more survivors than the list holds (W > 1024): every row
-  // (4) their second halves: 8 lanes per row, 4 rows per warp per round
-  unsigned long long key = 0ull;
-  for (int base = warp * 4; base < limit; base += 32) {
-    const int idx = base + quad;
-    int slot = -1;
-    if (idx < limit) slot = ns <= 1024 ? surv[idx] : idx;
-    float d2 = 0.f;
-    if (slot >= 0) d2 = dist8(qh, ld_stream(ring + (int64_t)slot * 16 + 8 + sub));
-    d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
-    d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
-    d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
-    if (slot >= 0 && sub == 0) {
-      const float pr = __ldcg(hpart + slot);
-      if (pr != CUDART_INF_F) {
-        const float d = pr + d2;
-        const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
-        const unsigned long long k2 =
-            ~(((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos));
-        key = k2 > key ? k2 : key;
+  float D = CUDART_INF_F;
+  for (int w = hl * wph; w < hl * wph + wph && w < 8; ++w) D = fminf(D, sD[w]);
+  // 3. other rows of the share that can still beat D*: 8 lanes per row, up to 8 rows per
+  //    lane group in flight (32 per warp per round; a fresh query makes every row survive)
+  if (active && D != CUDART_INF_F) {
+    for (int base = r0; base < r1; base += 32) {
+      const int slot = base + lane;
+      const float pr = slot < r1 ? __ldcg(hpart + slot) : CUDART_INF_F;
+      const bool surv = pr <= D && pr != CUDART_INF_F && slot != cs1 && slot != cs2;
+      unsigned mask = __ballot_sync(0xffffffffu, surv);
+      if (!mask) continue;
+      // lane group `quad` takes survivors quad, quad+4, quad+8, ... of this chunk
+      int li[8];
+      uint4 rv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        li[k] = -1;
+        int n = quad + 4 * k;  // the n-th set bit of mask
+        unsigned mm = mask;
+        for (; n > 0 && mm; --n) mm &= mm - 1;
+        if (mm) li[k] = __ffs(mm) - 1;
+        rv[k] = li[k] >= 0 ? ld_stream(ring + (int64_t)(base + li[k]) * 16 + 8 + sub) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float e = dist8(qh, rv[k]);
+        e += __shfl_xor_sync(0xffffffffu, e, 4);
+        e += __shfl_xor_sync(0xffffffffu, e, 2);
+        e += __shfl_xor_sync(0xffffffffu, e, 1);
+        const float prs = __shfl_sync(0xffffffffu, pr, li[k] >= 0 ? li[k] : 0);
+        if (li[k] >= 0 && sub == 0) {
+          const unsigned long long k2 = key_of(prs + e, base + li[k]);
+          key = k2 > key ? k2 : key;
+        }
       }
     }
   }
+  // 4. per head: exact argmin, decision; the group's plan
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
     key = other > key ? other : key;
   }
-  if (lane == 0) wkey[warp] = key;
+  if (lane == 0) skey[warp] = key;
   __syncthreads();
-  if (tid != 0) return;
-  for (int w = 1; w < 8; ++w) key = wkey[w] > key ? wkey[w] : key;
-  double bd = CUDART_INF;
-  int bpos = -1;
-  if (key) {
-    const unsigned long long raw = ~key;
-    bd = (double)__uint_as_float((unsigned)(raw >> 32));
-    bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
+  if (active && part == 0 && lane == 0) {
+    for (int w = hl * wph + 1; w < hl * wph + wph; ++w) key = skey[w] > key ? skey[w] : key;
+    double bd = CUDART_INF;
+    int bpos = -1;
+    if (key) {
+      const unsigned long long raw = ~key;
+      bd = (double)__uint_as_float((unsigned)(raw >> 32));
+      bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
+    }
+    slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
   }
-  decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos);
+  __syncthreads();
+  if (tid == 0) {
+    int lo_g = m;
+    for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
+    __threadfence();
+    plan_group(p, b, kvh, m, lo_g);
+  }
 }
 
 cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.batch * p.n_q_heads);
+  cfg.gridDim = dim3(p.batch * p.n_kv_heads);
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -344,7 +375,10 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;
   // the two-pass front covers the match stage only: append-only launches use the one-pass kernel
-  const FrontVariant& u = (v.two_pass && !do_match) ? kFrontVariants[1] : v;
+  // (verify_kernel gives each head 8/g warps: groups of up to 8 heads; with fewer groups than
+  // SMs, e.g. one long request, its one-CTA-per-group parallelism is too thin: one pass)
+  const bool two_pass = v.two_pass && do_match && p.n_q_heads / p.n_kv_heads <= 8 && p.batch * p.n_kv_heads >= 148;
+  const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
   u.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
   cudaError_t e = cudaGetLastError();
   if (e || !(u.two_pass && do_match)) return e;

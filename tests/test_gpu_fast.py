@@ -204,3 +204,38 @@ def test_step_graph_replay_equals_decode_step():
     assert hits > 0
     assert torch.equal(graphed.ring_acc[0], direct.ring_acc[0]) and torch.equal(graphed.ring_q[0], direct.ring_q[0])
     assert graphed.seq_lens[0].tolist() == [L] * B
+
+
+def test_two_pass_match_large_batch_replay():
+    """Enough GQA groups (B * Hkv >= 148) for the two-pass match (first-half scan + verify):
+    decisions identical and outputs within tolerance of the oracle, hits and misses mixed."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    L, B, hq, hkv, W, r = 120, 37, 16, 4, 64, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=300 + s,
+                                       rep_prob=0.7)) for s in range(B)]
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, L + 8, page_perm_seed=9, min_chunk=32)
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    oes = [orc.OracleEngine(ocfg, capacity=L + 8) for _ in range(B)]
+    q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)  # [L, B, H, d]
+    k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)
+    v = np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)
+    worst, hits, misses = 0.0, 0, 0
+    for m in range(1, L + 1):
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a[m - 1])).to("cuda", torch.bfloat16)  # noqa: E731
+        res = eng.decode_step(0, dev(q), dev(k), dev(v))
+        gh = res.match_hit.cpu().numpy().astype(bool)
+        gp = res.match_pos.cpu().numpy()
+        go = res.out.double().cpu().numpy()
+        for b in range(B):
+            st = oes[b].decode_step(0, q[m - 1, b], k[m - 1, b], v[m - 1, b], m)
+            np.testing.assert_array_equal(gh[b], st.hit)
+            np.testing.assert_array_equal(gp[b], st.p)
+            hits += int(st.use_hit.sum())
+            misses += int((~st.use_hit).sum())
+            if m % 10 == 0:
+                for h in range(hq):
+                    worst = max(worst, rel_err(go[b, h], st.outputs[h]))
+    assert hits > 0 and misses > 0
+    assert worst <= TOL, worst
