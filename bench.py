@@ -123,11 +123,12 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
     overstated; ncu's DRAM bytes cross-check it in profiles/)."""
     g = hq // hkv
     B = use.shape[0]
-    match = kv = summ = 0
+    match = verify = kv = summ = 0
     for b in range(B):
         live = min(int(m[b]) - 1, window)
-        if two_pass:
-            match += hq * live * (d // 2) * s_ring + hq * window * 4 * 2 + hq * d * s_ring
+        if two_pass:  # scan: first halves + partials written; verify: partials read back
+            match += hq * live * (d // 2) * s_ring + hq * window * 4 + hq * d * s_ring
+            verify += hq * window * 4
         else:
             match += hq * live * d * s_ring + hq * d * s_ring
         for j in range(hkv):
@@ -139,8 +140,8 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
     ring_w = B * hq * (d * s_ring + d * 4 + 4)
     out_w = B * hq * d * 4
     append = B * hkv * 2 * d * s_kv
-    return {"match": match, "amend": kv, "complete": summ + ring_w + out_w, "append": append,
-            "total": match + kv + summ + ring_w + out_w + append}
+    return {"match": match, "verify": verify, "amend": kv, "complete": summ + ring_w + out_w, "append": append,
+            "total": match + verify + kv + summ + ring_w + out_w + append}
 
 
 def full_bytes(m, hq, hkv, d, s_kv=2):
@@ -292,7 +293,7 @@ def run_ours(args, wl):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    stages = ("mac_append_kv", "mac_match", "mac_amend", "mac_complete")
+    stages = ("mac_append_kv", "mac_match_scan", "mac_match_verify", "mac_amend", "mac_complete")
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(S)]
     use_log = torch.empty(S, B, hq, dtype=torch.int32, device=dev)
     pos_log = torch.empty(S, B, hq, dtype=torch.int32, device=dev)
@@ -403,8 +404,8 @@ def run_ours(args, wl):
     stage_mean = stage_ms.mean(0)
     kern = {name: {"ms": float(stage_mean[i]), "bytes": mean_b[key],
                    "gbs": mean_b[key] / (stage_mean[i] * 1e-3) / 1e9}
-            for i, (name, key) in enumerate(zip(stages, ("append", "match", "amend", "complete")))}
-    dom = max(("mac_match", "mac_amend"), key=lambda n: kern[n]["bytes"])
+            for i, (name, key) in enumerate(zip(stages, ("append", "match", "verify", "amend", "complete")))}
+    dom = max(("mac_match_scan", "mac_amend"), key=lambda n: kern[n]["bytes"])
     step_gbs = mean_b["total"] / (ms_per_step * 1e-3) / 1e9
 
     result = None

@@ -150,6 +150,12 @@ int mac_amend_variant(const MacDecodeParams* p);
 
 int mac_append_kv(const MacDecodeParams* p, void* stream);
 int mac_match(const MacDecodeParams* p, void* stream);
+/* mac_match as its two passes (profiling; the bf16 d=128 path with >= 148 GQA groups):
+ * the ring scan (first-half distances) and the verification + decision + plan.  Where
+ * the match runs in one pass, mac_match_scan is the whole match and mac_match_verify is
+ * a no-op. */
+int mac_match_scan(const MacDecodeParams* p, void* stream);
+int mac_match_verify(const MacDecodeParams* p, void* stream);
 int mac_amend(const MacDecodeParams* p, void* stream);
 int mac_complete(const MacDecodeParams* p, void* stream);
 int mac_decode_step(const MacDecodeParams* p, void* stream);

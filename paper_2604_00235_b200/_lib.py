@@ -28,6 +28,8 @@ EXPORTS = (
     "mac_amend_variant",
     "mac_append_kv",
     "mac_match",
+    "mac_match_scan",
+    "mac_match_verify",
     "mac_amend",
     "mac_complete",
     "mac_decode_step",
@@ -135,7 +137,7 @@ def load() -> C.CDLL:
     lib.mac_workspace_bytes.argtypes = [C.POINTER(MacDecodeParams)]
     lib.mac_amend_variant.restype = C.c_int
     lib.mac_amend_variant.argtypes = [C.POINTER(MacDecodeParams)]
-    for name in ("mac_append_kv", "mac_match", "mac_amend", "mac_complete", "mac_decode_step", "mac_full_decode",
+    for name in ("mac_append_kv", "mac_match", "mac_match_scan", "mac_match_verify", "mac_amend", "mac_complete", "mac_decode_step", "mac_full_decode",
                  "mac_attend_full", "mac_shard_partial", "mac_shard_complete"):
         fn = getattr(lib, name)
         fn.restype = C.c_int

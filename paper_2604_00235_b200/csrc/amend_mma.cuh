@@ -31,6 +31,8 @@
 // out and the online-softmax state reset without draining the pipeline.
 #pragma once
 
+#include <type_traits>
+
 #include "complete.cuh"
 
 namespace mac {
@@ -97,6 +99,7 @@ struct State {
 
 // fold one 32-token step (two 16-token sub-tiles; this lane: 8 tokens of head `row`)
 // into the online-softmax state and accumulate P V.  vs1 == 0: second sub-tile absent.
+template <bool HAS1>
 __device__ __forceinline__ void softmax_pv(State& S, const float* l_in, const int* tok, int lo, int hi,
                                            uint32_t vs0, uint32_t vs1, int lane) {
   float l[8];
@@ -108,18 +111,24 @@ __device__ __forceinline__ void softmax_pv(State& S, const float* l_in, const in
   }
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-  const float Mn = fmaxf(S.M, mx);
+  // Lazy rescaling: the reference max M moves only when a logit exceeds it by more than
+  // 8 (log2 domain), so exp2(l - M) <= 256 stays exact in fp32 and in the bf16 hi/lo
+  // split, and the 64-multiply rescale of O runs only on those rare moves (never on the
+  // first tokens: O is still zero).  Z and O always share the same M, so acc = O / Z and
+  // lse = M ln2 + ln Z are unchanged.
+  const bool bump = mx > S.M + 8.f;
+  const float Mn = bump ? mx : S.M;
   float pv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float alpha = 1.f;
   if (Mn != -CUDART_INF_F) {
-    alpha = exp2f(S.M - Mn);
+    alpha = bump ? exp2f(S.M - Mn) : 1.f;
 #pragma unroll
     for (int e = 0; e < 8; ++e) pv[e] = exp2f(l[e] - Mn);
   }
+  const bool rescale = bump && S.M != -CUDART_INF_F;
   S.M = Mn;
   S.Z = S.Z * alpha + (((pv[0] + pv[1]) + (pv[2] + pv[3])) + ((pv[4] + pv[5]) + (pv[6] + pv[7])));
-  // rescale only when some row's running max moved (warp-uniform test)
-  if (__any_sync(0xffffffffu, alpha != 1.f)) {
+  if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
       S.o[nt][0] *= alpha; S.o[nt][1] *= alpha; S.o[nt][2] *= alpha; S.o[nt][3] *= alpha;
@@ -144,7 +153,7 @@ __device__ __forceinline__ void softmax_pv(State& S, const float* l_in, const in
     ldsm_x4_t(vs0 + swz(trow, 2 * j + (mi >> 1)), b0, b1, b2, b3);
     mma16816(S.o[2 * j], pa[0], b0, b1);
     mma16816(S.o[2 * j + 1], pa[0], b2, b3);
-    if (vs1) {
+    if (HAS1) {  // compile-time: no predicated ldmatrix (which costs a WARPSYNC + NOP each)
       uint32_t c0, c1, c2, c3;
       ldsm_x4_t(vs1 + swz(trow, 2 * j + (mi >> 1)), c0, c1, c2, c3);
       mma16816(S.o[2 * j], pa[1], c0, c1);
@@ -267,17 +276,19 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
   const int lo_piece = max(lo_h, t0), hi_piece = min(t1, cpos);
   const int lo_band = max(lo_h, max(t0, cpos + 1));
   // 32-token steps: sub-tiles 2jp and 2jp+1 (stages (2jp) % ST and (2jp+1) % ST)
-  const int nstep = (nsub + 1) >> 1;
-  for (int jp = 0; jp < nstep; ++jp) {
+  // 32-token steps over sub-tile pairs (2jp, 2jp+1); an odd tail sub-tile gets a half step.
+  // HAS1 is a template constant so the second sub-tile's ldmatrix is never predicated.
+  auto step = [&](int jp, auto has1_tag) {
+    constexpr bool HAS1 = decltype(has1_tag)::value;
     const int j0 = 2 * jp;
-    const bool has1 = j0 + 1 < nsub;
     cp_wait<ST - 2>();
     __syncwarp();
     const int ts = t0 + (jp << 5);
     const uint32_t ks0 = sm + (j0 % ST) * 2 * TILE_BYTES, vs0 = ks0 + TILE_BYTES;
     const uint32_t ks1 = sm + ((j0 + 1) % ST) * 2 * TILE_BYTES, vs1 = ks1 + TILE_BYTES;
-    // S = Q K^T for 4 n-tiles (32 tokens); even/odd k-steps accumulate separately
-    float s[4][2][4];  // k-steps 0 and 1 start the two chains with a zero accumulator
+    // S = Q K^T for 4 n-tiles (32 tokens); even/odd k-steps accumulate separately,
+    // k-steps 0 and 1 start the two chains with a zero accumulator
+    float s[4][2][4];
     {
       const int mi = lane >> 3, ii = lane & 7;
       const int trow = ((mi >> 1) << 3) + ii;
@@ -292,7 +303,7 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
           mma16816(s[0][ks & 1], qa[ks], b0, b1);
           mma16816(s[1][ks & 1], qa[ks], b2, b3);
         }
-        if (has1) {
+        if (HAS1) {
           uint32_t c0, c1, c2, c3;
           ldsm_x4(ks1 + swz(trow, 2 * ks + (mi & 1)), c0, c1, c2, c3);
           if (ks < 2) {
@@ -309,28 +320,37 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
     int tok[8];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
-      l[2 * nt] = ((s[nt][0][0] + s[nt][1][0]) + (s[nt][0][2] + s[nt][1][2])) * scale2;
-      l[2 * nt + 1] = ((s[nt][0][1] + s[nt][1][1]) + (s[nt][0][3] + s[nt][1][3])) * scale2;
+      if (!HAS1 && nt >= 2) {
+        l[2 * nt] = l[2 * nt + 1] = -CUDART_INF_F;
+      } else {
+        l[2 * nt] = ((s[nt][0][0] + s[nt][1][0]) + (s[nt][0][2] + s[nt][1][2])) * scale2;
+        l[2 * nt + 1] = ((s[nt][0][1] + s[nt][1][1]) + (s[nt][0][3] + s[nt][1][3])) * scale2;
+      }
       tok[2 * nt] = ts + nt * 8 + q4 * 2;
       tok[2 * nt + 1] = ts + nt * 8 + q4 * 2 + 1;
     }
-    const int hi_band = has1 ? t1 : min(t1, ts + 15);
-    if (ts <= hi_piece) softmax_pv(S, l, tok, lo_piece, has1 ? hi_piece : min(hi_piece, ts + 15), vs0,
-                                   has1 ? vs1 : 0u, lane);
-    if (ts + 31 > cpos && max(ts, cpos + 1) <= t1) {
+    const int hi_band = HAS1 ? t1 : min(t1, ts + 15);
+    // (the step's branches are warp-uniform; saying so through a vote lets ptxas drop the
+    // WARPSYNC it otherwise puts before every ldmatrix under them)
+    if (__any_sync(0xffffffffu, ts <= hi_piece))
+      softmax_pv<HAS1>(S, l, tok, lo_piece, HAS1 ? hi_piece : min(hi_piece, ts + 15), vs0, vs1, lane);
+    if (__any_sync(0xffffffffu, ts + 31 > cpos && max(ts, cpos + 1) <= t1)) {
       if (!in_band) {
         write_partial(S, out, 0, row, q4, g);
         S.reset();
         in_band = true;
       }
-      softmax_pv(S, l, tok, lo_band, hi_band, vs0, has1 ? vs1 : 0u, lane);
+      softmax_pv<HAS1>(S, l, tok, lo_band, hi_band, vs0, vs1, lane);
     }
     __syncwarp();
     if (j0 + ST < nsub) issue(j0 + ST, j0 % ST);
     cp_commit();
     if (j0 + 1 + ST < nsub) issue(j0 + 1 + ST, (j0 + 1) % ST);
     cp_commit();
-  }
+  };
+  const int npair = nsub >> 1;
+  for (int jp = 0; jp < npair; ++jp) step(jp, std::true_type{});
+  if (nsub & 1) step(npair, std::false_type{});
   cp_wait<0>();
   if (!in_band) {
     write_partial(S, out, 0, row, q4, g);

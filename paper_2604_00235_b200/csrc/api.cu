@@ -11,7 +11,7 @@ template <int MODE> cudaError_t launch_match_generic(const MacDecodeParams&, cud
 template <int MODE> cudaError_t launch_amend_generic(const MacDecodeParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_complete(const MacDecodeParams&, cudaStream_t, int);
 cudaError_t launch_front_bf16(const MacDecodeParams&, cudaStream_t, bool do_match, bool do_append, int rotate_only,
-                              int plan);
+                              int plan, int passes);
 cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t, int complete_mode);
 bool amend_mma_supported(const MacDecodeParams&);
 bool match_fast_supported(const MacDecodeParams&);
@@ -45,14 +45,16 @@ static int validate(const MacDecodeParams* p, bool need_ring) {
 
 enum : int {
   STAGE_APPEND = 1,         // append K/V at m = seq_lens + 1, rotate q
-  STAGE_MATCH = 2,          // ring match + decision + plan
+  STAGE_MATCH = 2,          // ring match + decision + plan (both passes of the two-pass match)
   STAGE_AMEND = 4,          // split-KV partials over the plan
   STAGE_COMPLETE = 8,       // merge, output, ring write-back
   STAGE_COMPLETE_FULL = 16, // merge and output only (full-attention modes)
   STAGE_ROTATE = 32,        // rotate q at m = seq_lens, no append
   STAGE_PLAN_FULL = 64,     // plan every group as [1, m] in the append stage
   STAGE_EXPORT = 128,       // this KV shard's (piece, band) partials -> shard_out
-  STAGE_SHARDS = 256        // merge the gathered shard partials, output, ring write-back
+  STAGE_SHARDS = 256,       // merge the gathered shard partials, output, ring write-back
+  STAGE_SCAN_ONLY = 512,    // with STAGE_MATCH: pass 1 only (profiling)
+  STAGE_VERIFY_ONLY = 1024  // with STAGE_MATCH: pass 2 only (profiling)
 };
 
 template <int MODE>
@@ -62,8 +64,9 @@ static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int mask)
   const int rot = (mask & STAGE_ROTATE) ? 1 : 0, plan = (mask & STAGE_PLAN_FULL) ? 1 : 0;
   if (MODE == MAC_MODE_BF16 && front_fast_supported(p)) {
     const bool fast_match = (mask & STAGE_MATCH) && match_fast_supported(p);
+    const int passes = (mask & STAGE_SCAN_ONLY) ? 1 : ((mask & STAGE_VERIFY_ONLY) ? 2 : 3);
     if (app || fast_match) {
-      e = launch_front_bf16(p, st, fast_match, app, rot, plan);
+      e = launch_front_bf16(p, st, fast_match, app && passes != 2, rot, plan, passes);
       if (e) return e;
     }
     if ((mask & STAGE_MATCH) && !fast_match) { e = launch_match_generic<MODE>(p, st); if (e) return e; }
@@ -130,6 +133,12 @@ int mac_amend_variant(const MacDecodeParams* p) {
 
 int mac_append_kv(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_APPEND, false); }
 int mac_match(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_MATCH, true); }
+int mac_match_scan(const MacDecodeParams* p, void* stream) {
+  return dispatch(p, stream, STAGE_MATCH | STAGE_SCAN_ONLY, true);
+}
+int mac_match_verify(const MacDecodeParams* p, void* stream) {
+  return dispatch(p, stream, STAGE_MATCH | STAGE_VERIFY_ONLY, true);
+}
 int mac_amend(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_AMEND, true); }
 int mac_complete(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_COMPLETE, true); }
 int mac_decode_step(const MacDecodeParams* p, void* stream) {

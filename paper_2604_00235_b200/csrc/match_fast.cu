@@ -362,8 +362,9 @@ static const FrontVariant kFrontVariants[] = {
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
+// passes: bit 0 = the scan (append, rows), bit 1 = the verify kernel (two-pass mode only)
 cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append,
-                              int rotate_only, int plan) {
+                              int rotate_only, int plan, int passes) {
   static int vi = -1;
   if (vi < 0) {
     const char* env = getenv("MAC_FRONT_VARIANT");
@@ -379,10 +380,13 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   // SMs, e.g. one long request, its one-CTA-per-group parallelism is too thin: one pass)
   const bool two_pass = v.two_pass && do_match && p.n_q_heads / p.n_kv_heads <= 8 && p.batch * p.n_kv_heads >= 148;
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
-  u.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
-  cudaError_t e = cudaGetLastError();
-  if (e || !(u.two_pass && do_match)) return e;
-  return launch_verify(p, st);
+  if (passes & 1) {
+    u.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
+    const cudaError_t e = cudaGetLastError();
+    if (e) return e;
+  }
+  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st);
+  return cudaSuccess;
 }
 
 }  // namespace mac

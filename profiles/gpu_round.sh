@@ -11,11 +11,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 600 python bench.py --workload c4 --steps 10 --warmup 3 > $O/bench_c4.json 2> $O/bench_c4.err
-KERN='regex:front_|append_rope|match_|amend_|complete_'
+KERN='regex:front_|append_rope|match_|verify|amend_|complete_'
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -k "$KERN" -c 60 --csv --log-file $O/launches.csv \
   python bench.py --steps 4 --warmup 3 --no-cpu --full-steps 3 > $O/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "$KERN" -s 9 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k "$KERN" -s 12 -c 4 \
   -o $O/prof -f python bench.py --steps 4 --warmup 3 --no-cpu --full-steps 3 > $O/ncu_full.log 2>&1
 timeout 1800 python sweep.py --out $O/sweep.jsonl > $O/sweep.log 2>&1
 ls -la $O
