@@ -45,12 +45,6 @@ __global__ void __launch_bounds__(128) amend_generic_kernel(MacDecodeParams p, c
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
   const kv_t* kc = static_cast<const kv_t*>(p.k_cache);
   const kv_t* vc = static_cast<const kv_t*>(p.v_cache);
-  {  // this path splits by (split, group) directly: retire the plan's work-list slots
-    const Workspace w = workspace_layout(p);
-    const unsigned n_list = __ldcg(ws_ptr<unsigned int>(p, w.ctr_off));
-    int4* list = ws_ptr<int4>(p, w.list_off);
-    for (unsigned i = blockIdx.x * blockDim.x + tid; i < n_list; i += gridDim.x * blockDim.x) list[i].x = 0;
-  }
 
   for (long v = blockIdx.x; v < total; v += gridDim.x) {
     const int c = (int)(v / G), grp = (int)(v % G);

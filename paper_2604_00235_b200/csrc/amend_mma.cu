@@ -22,7 +22,7 @@ __device__ __forceinline__ void amend_retire(unsigned int* ctr, int complete_mod
   __threadfence();
   const unsigned prev = atomicAdd(ctr + 2, 1u);
   if (prev == gridDim.x - 1) {
-    if (complete_mode) ctr[0] = ctr[5] = 0u;  // fused complete: the work list is fully consumed
+    if (complete_mode) ctr[0] = 0u;  // fused complete: the work list is fully consumed
     ctr[1] = 0u;
     ctr[2] = 0u;
   }
@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, 
     if (item >= n_items) break;
     int4 it = next_it;
     it.x -= 1;
-    if (lane == 0) list[item].x = 0;  // consumed: the slot is empty for the next step
     unsigned nx = 0;
     if (lane == 0) nx = atomicAdd(ctr + 1, 1u);
     next = __reduce_max_sync(0xffffffffu, nx);

@@ -47,9 +47,6 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
       qrot[qi + 1] = (acc_t)(x0 * s + x1 * c);
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) st_release_u32(ws_ptr<unsigned int>(p, workspace_layout(p).app_off) + blockIdx.x, (unsigned)m);
   if (plan && threadIdx.x == 0) {  // full-attention modes: every head reads [1, m]
     int* lo = ws_ptr<int>(p, workspace_layout(p).lo_off);
     for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;

@@ -107,14 +107,6 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -194,14 +186,13 @@ struct Workspace {
   size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
   size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
   size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter, 2 amend done counter,
-                     //              5 groups planned, 7 error flag (a bounded wait gave up)
+                     //              (3-15 spare)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  splits planned for the group
   size_t mpos_off;   // [B] i32      position m of this step
-  size_t app_off;    // [B*Hkv] u32  position the group's append landed at (release flag)
   size_t lo_off;     // [B*Hq] i32   first token each head reads (plan)
-  size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp + 1, c, t0, t1}; x = 0: empty
-                     //              slot (x is the slot's ready flag; consumers zero it)
+  size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp + 1, c, t0, t1} (the amend
+                     //              kernel reads them after the plan is complete; x = 0: empty)
   size_t qrot_off;   // [B*Hq*d]     rotated queries (math dtype)
   size_t part_off;   // [B*Hq*max_chunks*2*(d_v+1)] split partial summaries
   size_t hpart_off;  // [B*Hq*W] f32  two-pass match: distance over the first d/2 dims per ring row
@@ -220,8 +211,7 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.gdone_off = align256(w.ctr_off + 64);
   w.pn_off = align256(w.gdone_off + 4 * groups);
   w.mpos_off = align256(w.pn_off + 4 * groups);
-  w.app_off = align256(w.mpos_off + 4 * (size_t)p.batch);
-  w.lo_off = align256(w.app_off + 4 * groups);
+  w.lo_off = align256(w.mpos_off + 4 * (size_t)p.batch);
   w.list_off = align256(w.lo_off + 4 * rows);
   w.qrot_off = align256(w.list_off + 16 * groups * p.max_chunks);
   w.part_off = align256(w.qrot_off + acc * rows * p.head_dim);
@@ -251,15 +241,8 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
   const int n = (int)min((unsigned)ch.n, base < cap ? cap - base : 0u);  // full list: cannot happen
   for (int c = 0; c < n; ++c) {
     const int t0 = start + c * ch.len;
-    int4* e = list + base + c;
-    e->y = c;
-    e->z = t0;
-    e->w = min(end, t0 + ch.len - 1);
+    list[base + c] = make_int4(grp + 1, c, t0, min(end, t0 + ch.len - 1));
   }
-  // publish: one fence, then the x words (grp + 1), each slot's ready flag
-  __threadfence();
-  for (int c = 0; c < n; ++c) list[base + c].x = grp + 1;
-  atom_add_acq_rel(ctr + 5, 1u);  // groups planned: the list is final once this reaches B*Hkv
 }
 
 // Decide one (request, q head) from its best candidate and apply the gates;

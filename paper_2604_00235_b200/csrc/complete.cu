@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, int fu
   if (bh < p.batch * p.n_q_heads) complete_head<MODE>(p, bh, full_mode);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // work list consumed
     unsigned int* ctr = ws_ptr<unsigned int>(p, workspace_layout(p).ctr_off);
-    ctr[0] = ctr[5] = 0u;
+    ctr[0] = 0u;
   }
 }
 

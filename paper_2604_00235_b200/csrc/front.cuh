@@ -48,11 +48,6 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
     for (int e = lane; e < 128; e += 32)
       vc[row * 128 + e] =
           from_f64<__nv_bfloat16>(load_in(p.v_in, ((int64_t)b * p.n_kv_heads + kvh) * 128 + e, p.in_dtype));
-  // "group appended at m" for amend workers that run concurrently with this kernel:
-  // every lane's stores are fenced before lane 0's release store
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release_u32(ws_ptr<unsigned int>(p, w.app_off) + idx, (unsigned)m);
   if (plan && lane == 0) {
     int* lo = ws_ptr<int>(p, w.lo_off);
     for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;
