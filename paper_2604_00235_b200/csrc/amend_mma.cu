@@ -18,18 +18,17 @@ bool amend_mma_supported(const MacDecodeParams& p) {
 }
 
 // last warp out resets the queue counters for the next step
-__device__ __forceinline__ void amend_retire(unsigned int* ctr, int complete_mode) {
+__device__ __forceinline__ void amend_retire(unsigned int* ctr) {
   __threadfence();
   const unsigned prev = atomicAdd(ctr + 2, 1u);
   if (prev == gridDim.x - 1) {
-    if (complete_mode) ctr[0] = 0u;  // fused complete: the work list is fully consumed
     ctr[1] = 0u;
     ctr[2] = 0u;
   }
 }
 
 template <int ST, int MINB>  // cp.async stages per warp, min resident warps per SM (register budget)
-__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, int complete_mode) {
+__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) {
   // programmatic dependent launch: wait for the front kernel's plan before touching it
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // and let the complete kernel's grid launch as amend warps retire
@@ -59,16 +58,14 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, 
     unsigned nx = 0;
     if (lane == 0) nx = atomicAdd(ctr + 1, 1u);
     next = __reduce_max_sync(0xffffffffu, nx);
-    const int grp = (int)__reduce_max_sync(0xffffffffu, (unsigned)it.x);
     amend_mma_item<ST>(p, it, sm, [&]() { if (next < n_items) next_it = __ldcg(list + next); });
-    if (complete_mode) amend_group_done(p, grp, complete_mode);
   }
-  if (lane == 0) amend_retire(ctr, complete_mode);
+  if (lane == 0) amend_retire(ctr);
 }
 
 // Variants (stages, min warps per SM); MAC_AMEND_VARIANT selects one (development knob).
 struct AmendVariant {
-  void (*fn)(MacDecodeParams, int);
+  void (*fn)(MacDecodeParams);
   int smem;
 };
 static const AmendVariant kAmendVariants[] = {
@@ -77,7 +74,7 @@ static const AmendVariant kAmendVariants[] = {
     {amend_mma_kernel<2, 8>, 2 * 2 * TILE_BYTES},
 };
 
-cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, int complete_mode) {
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st) {
   static int grid_full = 0, vi = 0;
   if (!grid_full) {
     const char* env = getenv("MAC_AMEND_VARIANT");
@@ -106,7 +103,7 @@ cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, int
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, v.fn, p, complete_mode);
+  return cudaLaunchKernelEx(&cfg, v.fn, p);
 }
 
 }  // namespace mac

@@ -359,29 +359,4 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
   write_partial(S, out, 1, row, q4, g);
 }
 
-// Count one finished split of group `grp`; the warp landing the group's last
-// split completes the group's heads (K3 fused: merge, output, ring write-back).
-// complete_mode 1: decode step, 2: full attention.
-static __device__ __noinline__ void amend_group_done(const MacDecodeParams& p, int grp, int complete_mode) {
-  const int lane = threadIdx.x & 31;
-  const Workspace w = workspace_layout(p);
-  unsigned int* gdone = ws_ptr<unsigned int>(p, w.gdone_off);
-  const int* plan_n = ws_ptr<const int>(p, w.pn_off);
-  const int Hkv = p.n_kv_heads, Hq = p.n_q_heads, g = Hq / Hkv;
-  const int b = grp / Hkv, kvh = grp % Hkv;
-  unsigned last = 0;
-  __syncwarp();
-  if (lane == 0) {
-    const unsigned prev = atom_add_acq_rel(gdone + grp, 1u);
-    last = prev + 1 == (unsigned)plan_n[grp];
-    if (last) gdone[grp] = 0u;
-  }
-  last = __reduce_max_sync(0xffffffffu, last);
-  if (last) {
-    __threadfence();
-    const int mode = complete_mode == 2 ? COMPLETE_FULL : COMPLETE_RING;
-    for (int j = 0; j < g; ++j) complete_head<MAC_MODE_BF16>(p, b * Hq + kvh * g + j, mode);
-  }
-}
-
 }  // namespace mac

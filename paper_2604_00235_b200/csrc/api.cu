@@ -12,7 +12,7 @@ template <int MODE> cudaError_t launch_amend_generic(const MacDecodeParams&, cud
 template <int MODE> cudaError_t launch_complete(const MacDecodeParams&, cudaStream_t, int);
 cudaError_t launch_front_bf16(const MacDecodeParams&, cudaStream_t, bool do_match, bool do_append, int rotate_only,
                               int plan, int passes);
-cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t, int complete_mode);
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t);
 bool amend_mma_supported(const MacDecodeParams&);
 bool match_fast_supported(const MacDecodeParams&);
 bool front_fast_supported(const MacDecodeParams&);
@@ -75,18 +75,12 @@ static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int mask)
     if (mask & STAGE_MATCH) { e = launch_match_generic<MODE>(p, st); if (e) return e; }
   }
   const bool fast_amend = MODE == MAC_MODE_BF16 && amend_mma_supported(p);
-  // the tensor-core amend completes each group in its tail when the step asks for
-  // amend and complete together (mac_decode_step / mac_full_decode)
-  static const int fuse_ok = getenv("MAC_FUSE_COMPLETE") ? atoi(getenv("MAC_FUSE_COMPLETE")) : 0;  // measured slower
-  const int fused = (fuse_ok && fast_amend && (mask & STAGE_AMEND) && !(mask & STAGE_EXPORT))
-                        ? ((mask & STAGE_COMPLETE) ? 1 : ((mask & STAGE_COMPLETE_FULL) ? 2 : 0))
-                        : 0;
   if (mask & STAGE_AMEND) {
-    if (fast_amend) e = launch_amend_mma_bf16(p, st, fused);
+    if (fast_amend) e = launch_amend_mma_bf16(p, st);
     else e = launch_amend_generic<MODE>(p, st);
     if (e) return e;
   }
-  if (!fused) {
+  {
     if (mask & STAGE_COMPLETE) { e = launch_complete<MODE>(p, st, 0); if (e) return e; }
     if (mask & STAGE_COMPLETE_FULL) { e = launch_complete<MODE>(p, st, 1); if (e) return e; }
     if (mask & STAGE_EXPORT) { e = launch_complete<MODE>(p, st, 2); if (e) return e; }
