@@ -72,26 +72,34 @@ static const AmendVariant kAmendVariants[] = {
     {amend_mma_kernel<4, 7>, 4 * 2 * TILE_BYTES},
     {amend_mma_kernel<6, 4>, 6 * 2 * TILE_BYTES},
     {amend_mma_kernel<2, 8>, 2 * 2 * TILE_BYTES},
+    {amend_mma_kernel<3, 8>, 3 * 2 * TILE_BYTES},
 };
 
-cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st) {
-  static int grid_full = 0, vi = 0;
-  if (!grid_full) {
+// full_spans: every group reads [1, m] (full-attention decode and its miss path), where
+// the 3-stage / 8-warps-per-SM variant measured best (C3: 2.41 vs 2.53 ms); the hit path's
+// short spans prefer 4 stages at 6 warps per SM (81.0 vs 84.5 us).  MAC_AMEND_VARIANT
+// overrides both.
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, bool full_spans) {
+  constexpr int kN = (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0]));
+  static int grid_full[kN] = {}, forced = -2;
+  if (forced == -2) {
     const char* env = getenv("MAC_AMEND_VARIANT");
-    vi = env ? atoi(env) : 0;
-    if (vi < 0 || vi >= (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0]))) vi = 0;
-    const AmendVariant& v = kAmendVariants[vi];
+    forced = env ? atoi(env) : -1;
+    if (forced >= kN) forced = -1;
+  }
+  const int vi = forced >= 0 ? forced : (full_spans ? 3 : 0);
+  const AmendVariant& v = kAmendVariants[vi];
+  if (!grid_full[vi]) {
     cudaError_t e = cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, 32, v.smem);
-    grid_full = sms * (per_sm < 1 ? 1 : per_sm);
+    grid_full[vi] = sms * (per_sm < 1 ? 1 : per_sm);
   }
-  const AmendVariant& v = kAmendVariants[vi];
   const long cap = (long)p.batch * p.n_kv_heads * p.max_chunks;
-  const int grid = (int)(grid_full < cap ? grid_full : cap);
+  const int grid = (int)(grid_full[vi] < cap ? grid_full[vi] : cap);
   // programmatic dependent launch: the grid is set up while the front kernel drains
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

@@ -12,7 +12,7 @@ template <int MODE> cudaError_t launch_amend_generic(const MacDecodeParams&, cud
 template <int MODE> cudaError_t launch_complete(const MacDecodeParams&, cudaStream_t, int);
 cudaError_t launch_front_bf16(const MacDecodeParams&, cudaStream_t, bool do_match, bool do_append, int rotate_only,
                               int plan, int passes);
-cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t);
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams&, cudaStream_t, bool full_spans);
 bool amend_mma_supported(const MacDecodeParams&);
 bool match_fast_supported(const MacDecodeParams&);
 bool front_fast_supported(const MacDecodeParams&);
@@ -76,7 +76,7 @@ static cudaError_t run_step(const MacDecodeParams& p, cudaStream_t st, int mask)
   }
   const bool fast_amend = MODE == MAC_MODE_BF16 && amend_mma_supported(p);
   if (mask & STAGE_AMEND) {
-    if (fast_amend) e = launch_amend_mma_bf16(p, st);
+    if (fast_amend) e = launch_amend_mma_bf16(p, st, plan != 0);
     else e = launch_amend_generic<MODE>(p, st);
     if (e) return e;
   }
