@@ -346,7 +346,7 @@ def run_ours(args, wl):
     use = use_log.cpu().numpy()
     pos = pos_log.cpu().numpy()
     mm = m_log.cpu().numpy()
-    two_pass = os.environ.get("MAC_FRONT_VARIANT", "0") == "0"
+    two_pass = os.environ.get("MAC_FRONT_VARIANT", "0") in ("0", "4", "5")
     byts = [step_bytes(use[s], pos[s], mm[s], hq, hkv, D, WINDOW, BAND, two_pass=two_pass) for s in range(W_, S)]
     hit_rate = float(use[W_:].mean())
 

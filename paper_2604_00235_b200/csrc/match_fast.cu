@@ -132,9 +132,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(M
 // ring bytes; when nearly every row survives (a fresh query, all distances
 // ~2d) pass 2 reads the second halves of all rows — the one-pass bytes.  The
 // distance is the one-pass kernel's fp32 sum of squares split in two sums.
-__global__ void __launch_bounds__(kThreads, 5) front_half_kernel(MacDecodeParams p, int n_match, int do_append,
-                                                                 int rotate_only, int plan, int /*unused*/) {
-  constexpr int kRowsPerCta = 128, kLoads = kRowsPerCta / 32;  // 8 lanes per row, 4 rows per warp-load
+template <int kRowsPerCta, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDecodeParams p, int n_match,
+                                                                          int do_append, int rotate_only, int plan,
+                                                                          int /*unused*/) {
+  constexpr int kLoads = kRowsPerCta / 32;  // 8 lanes per row, 4 rows per warp-load
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -345,8 +347,9 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-// MAC_FRONT_VARIANT (development knob): 0 = two-pass match (default), 1-3 = one-pass stream with
-// (ring rows per CTA, min CTAs per SM) = (128,5), (64,8), (256,3).  Measured alternatives that lost on C3 (persistent tensor-core, persistent
+// MAC_FRONT_VARIANT (development knob): two-pass match with (ring rows per CTA, min CTAs per
+// SM) = 0: (256,4) default, 4: (128,5), 5: (64,8); one-pass stream 1-3: (128,5), (64,8), (256,3).
+// C3 step: 76.2 / 81.0 / 93.8 us two-pass, 95.6 us one-pass (128,5).  Measured alternatives that lost on C3 (persistent tensor-core, persistent
 // CUDA-core, f32x2 "lean", DSMEM-cluster argmin, one fused step kernel) are on branch
 // exp/fused-step; numbers in DESIGN.md §4.
 struct FrontVariant {
@@ -355,10 +358,12 @@ struct FrontVariant {
   bool two_pass;  // front_half_kernel + verify_kernel
 };
 static const FrontVariant kFrontVariants[] = {
-    {front_half_kernel, 128, true},
+    {front_half_kernel<256, 4>, 256, true},
     {front_bf16_d128_kernel<128, 5>, 128, false},
     {front_bf16_d128_kernel<64, 8>, 64, false},
     {front_bf16_d128_kernel<256, 3>, 256, false},
+    {front_half_kernel<128, 5>, 128, true},
+    {front_half_kernel<64, 8>, 64, true},
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
