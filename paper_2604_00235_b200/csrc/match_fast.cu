@@ -114,6 +114,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(M
   publish_and_decide(p, bh, m, n_scan, nsplit, key);
 }
 
+// packed fp32 pairs (Blackwell FFMA2): two lanes of fp32 math per instruction
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+// sum over 8 dims of (q - c)^2, the bf16 row chunk c against the query pairs q2: per element
+// pair one FFMA2 for q - c (exactly rounded, c * -1 + q) and one for the square-accumulate
+__device__ __forceinline__ float dist8_f2(const unsigned long long* q2, uint4 c) {
+  const unsigned long long neg1 = f2_pack(-1.f, -1.f);
+  unsigned long long acc = 0ull;
+  const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long cc = f2_pack(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
+    const unsigned long long e = f2_fma(cc, neg1, q2[i]);
+    acc = f2_fma(e, e, acc);
+  }
+  return __uint_as_float((unsigned)acc) + __uint_as_float((unsigned)(acc >> 32));
+}
+
 // ---------------------------------------------------------------------------
 // Two-pass match (default for the bf16 d=128 decode step).
 //
@@ -159,26 +183,45 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
     const int slot = row0 + k * 32 + warp * 4 + quad;
     v[k] = slot < W ? ld_stream(ring + (int64_t)slot * 16 + sub) : make_uint4(0, 0, 0, 0);
   }
-  float q[8];
+  unsigned long long q2[4];  // this lane's 8 first-half query dims, as fp32 pairs
 #pragma unroll
-  for (int i = 0; i < 8; ++i) q[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + sub * 8 + i, p.in_dtype);
+  for (int i = 0; i < 4; ++i)
+    q2[i] = f2_pack((float)load_in(p.q_pre, (int64_t)bh * 128 + sub * 8 + 2 * i, p.in_dtype),
+                    (float)load_in(p.q_pre, (int64_t)bh * 128 + sub * 8 + 2 * i + 1, p.in_dtype));
   int first = m - W;
   if (first < 1) first = 1;
   if (p.delta_max > 0 && m - p.delta_max > first) first = m - p.delta_max;
   const int last = m - 1;
   const int cur_slot = last >= 1 ? (last - 1) % W : 0;
   float* hpart = ws_ptr<float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
+  float part[kLoads];
 #pragma unroll
-  for (int k = 0; k < kLoads; ++k) {
-    const int slot = row0 + k * 32 + warp * 4 + quad;
-    float d = dist8(q, v[k]);
-    d += __shfl_xor_sync(0xffffffffu, d, 4);
-    d += __shfl_xor_sync(0xffffffffu, d, 2);
-    d += __shfl_xor_sync(0xffffffffu, d, 1);
-    const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
-    const bool live = slot < W && last >= 1 && pos >= first;
-    if (sub == 0 && slot < W) hpart[slot] = live ? d : CUDART_INF_F;  // dead rows: +inf, never survive
+  for (int k = 0; k < kLoads; ++k) part[k] = dist8_f2(q2, v[k]);
+  // reduce-scatter over the row's 8 lanes (kLoads = 8: one shuffle per row instead of
+  // three): after the xor-4, -2, -1 rounds lane `sub` holds the full partial of row k = sub
+  static_assert(kLoads == 8 || kLoads == 4 || kLoads == 2, "reduce-scatter layout");
+#pragma unroll
+  for (int o = 4, n = kLoads; o > 0; o >>= 1) {
+    if (n > 1) {
+      const bool up = sub & o;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const float send = up ? part[i] : part[i + n / 2];
+        const float keep = up ? part[i + n / 2] : part[i];
+        part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      n >>= 1;
+    } else {
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], o);
+    }
   }
+  // lane `sub` now holds row k = sub >> (3 - log2(kLoads)) (kLoads < 8: lanes pair up)
+  constexpr int kShift = kLoads == 8 ? 0 : (kLoads == 4 ? 1 : 2);
+  const int k = sub >> kShift;
+  const int slot = row0 + k * 32 + warp * 4 + quad;
+  const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
+  const bool live = slot < W && last >= 1 && pos >= first;
+  if ((sub & ((1 << kShift) - 1)) == 0 && slot < W) hpart[slot] = live ? part[0] : CUDART_INF_F;
 }
 
 // Pass 2: one CTA per GQA group (request, kv head), 8 warps: 8/g warps per head,
@@ -377,14 +420,14 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
     if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
   }
   const FrontVariant& v = kFrontVariants[vi];
-  const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + v.rows - 1) / v.rows) : 0;
-  const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
-  if (n_match + n_append == 0) return cudaSuccess;
   // the two-pass front covers the match stage only: append-only launches use the one-pass kernel
   // (verify_kernel gives each head 8/g warps: groups of up to 8 heads; with fewer groups than
   // SMs, e.g. one long request, its one-CTA-per-group parallelism is too thin: one pass)
   const bool two_pass = v.two_pass && do_match && p.n_q_heads / p.n_kv_heads <= 8 && p.batch * p.n_kv_heads >= 148;
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
+  const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
+  const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
+  if (n_match + n_append == 0) return cudaSuccess;
   if (passes & 1) {
     u.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
