@@ -262,15 +262,26 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   auto key_of = [&](float d, int slot) {
     return ~(((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos_of(slot)));
   };
+  // every partial of this lane's share, all loads in flight at once (a share is at most
+  // W <= 1024 rows, launch_front_bf16 checks); L1-allocating loads, so the survivor pass
+  // below re-reads them from L1
+  constexpr int kPer = 32;
+  float prv[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int slot = r0 + i * 32 + lane;
+    prv[i] = (active && slot < r1) ? hpart[slot] : CUDART_INF_F;
+  }
   // 1. two smallest partials of this warp's share
   float p1 = CUDART_INF_F, p2 = CUDART_INF_F;
   int s1 = -1, s2 = -1;
-  if (active)
-    for (int slot = r0 + lane; slot < r1; slot += 32) {
-      const float pr = __ldcg(hpart + slot);
-      if (pr < p1) { p2 = p1; s2 = s1; p1 = pr; s1 = slot; }
-      else if (pr < p2) { p2 = pr; s2 = slot; }
-    }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const float pr = prv[i];
+    const int slot = r0 + i * 32 + lane;
+    if (pr < p1) { p2 = p1; s2 = s1; p1 = pr; s1 = slot; }
+    else if (pr < p2) { p2 = pr; s2 = slot; }
+  }
   float c1 = p1;
   int cs1 = s1;
 #pragma unroll
@@ -310,9 +321,10 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   // 3. other rows of the share that can still beat D*: 8 lanes per row, up to 8 rows per
   //    lane group in flight (32 per warp per round; a fresh query makes every row survive)
   if (active && D != CUDART_INF_F) {
+#pragma unroll 1
     for (int base = r0; base < r1; base += 32) {
       const int slot = base + lane;
-      const float pr = slot < r1 ? __ldcg(hpart + slot) : CUDART_INF_F;
+      const float pr = slot < r1 ? hpart[slot] : CUDART_INF_F;
       const bool surv = pr <= D && pr != CUDART_INF_F && slot != cs1 && slot != cs2;
       unsigned mask = __ballot_sync(0xffffffffu, surv);
       if (!mask) continue;
@@ -423,7 +435,8 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   // the two-pass front covers the match stage only: append-only launches use the one-pass kernel
   // (verify_kernel gives each head 8/g warps: groups of up to 8 heads; with fewer groups than
   // SMs, e.g. one long request, its one-CTA-per-group parallelism is too thin: one pass)
-  const bool two_pass = v.two_pass && do_match && p.n_q_heads / p.n_kv_heads <= 8 && p.batch * p.n_kv_heads >= 148;
+  const bool two_pass = v.two_pass && do_match && p.n_q_heads / p.n_kv_heads <= 8 && p.batch * p.n_kv_heads >= 148 &&
+                        p.window <= 1024;
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
