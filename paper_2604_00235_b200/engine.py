@@ -368,7 +368,9 @@ class StepGraph:
     position from `seq_lens`, every workspace counter returns to zero by the end of the
     step), so one graph serves every step of the layer."""
 
-    def __init__(self, eng: "BatchDecodeEngine", layer: int, dtype=torch.bfloat16):
+    def __init__(self, eng: "BatchDecodeEngine", layer: int, dtype=torch.bfloat16, out_dtype=None):
+        """dtype: the q/k/v input dtype; out_dtype: the host output dtype (default the engine's
+        summary dtype, f32 for bf16 storage; bf16 halves the device-to-host bytes)."""
         cfg, B = eng.cfg, eng.batch
         eng._layer(layer)
         self.eng, self.layer = eng, layer
@@ -381,7 +383,10 @@ class StepGraph:
                            t[nq + nk:].view(B, cfg.n_kv_heads, cfg.d_v))
         self.q_host, self.k_host, self.v_host = split(self.in_host)
         self.q_dev, self.k_dev, self.v_dev = split(self.in_dev)
-        self.out_host = torch.zeros(B, cfg.n_q_heads, cfg.d_v, dtype=eng.sumdt).pin_memory()
+        self.out_dtype = out_dtype or eng.sumdt
+        self.out_host = torch.zeros(B, cfg.n_q_heads, cfg.d_v, dtype=self.out_dtype).pin_memory()
+        self.out_dev = (torch.zeros(B, cfg.n_q_heads, cfg.d_v, dtype=self.out_dtype, device=dev)
+                        if self.out_dtype != eng.sumdt else None)
         self.graph = torch.cuda.CUDAGraph()
         self.h2d_bytes = self.in_host.numel() * self.in_host.element_size()
         self.d2h_bytes = self.out_host.numel() * self.out_host.element_size()
@@ -396,7 +401,11 @@ class StepGraph:
         eng = self.eng
         self.in_dev.copy_(self.in_host, non_blocking=True)
         eng.decode_step(self.layer, self.q_dev, self.k_dev, self.v_dev)
-        self.out_host.copy_(eng.o_out, non_blocking=True)
+        if self.out_dev is not None:  # narrowed on the device first: fewer bytes over the host link
+            self.out_dev.copy_(eng.o_out)
+            self.out_host.copy_(self.out_dev, non_blocking=True)
+        else:
+            self.out_host.copy_(eng.o_out, non_blocking=True)
 
     def replay(self):
         self.graph.replay()

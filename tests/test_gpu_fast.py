@@ -189,7 +189,9 @@ def test_step_graph_replay_equals_decode_step():
     cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=64, band=16, storage="bf16")
     direct = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
     graphed = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    narrow = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
     sg = StepGraph(graphed, 0)
+    sg16 = StepGraph(narrow, 0, out_dtype=torch.bfloat16)
     hits = 0
     for m in range(1, L + 1):
         res = direct.decode_step(0, q[m - 1].cuda(), k[m - 1].cuda(), v[m - 1].cuda())
@@ -197,8 +199,12 @@ def test_step_graph_replay_equals_decode_step():
         sg.k_host.copy_(k[m - 1])
         sg.v_host.copy_(v[m - 1])
         sg.replay()
+        for dst, src in ((sg16.q_host, q), (sg16.k_host, k), (sg16.v_host, v)):
+            dst.copy_(src[m - 1])
+        sg16.replay()
         torch.cuda.synchronize()
         assert torch.equal(sg.out_host, res.out.cpu()), m
+        assert torch.equal(sg16.out_host, res.out.cpu().bfloat16()), m
         assert torch.equal(graphed.o_pos, direct.o_pos)
         hits += int(direct.o_use.sum())
     assert hits > 0
