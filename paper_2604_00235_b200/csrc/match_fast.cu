@@ -233,14 +233,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 //      P(r) <= D* (usually none on the hit path);
 //   4. per head: exact argmin over candidates and survivors, decide_one; the
 //      group is planned in the same CTA (no cross-CTA arrival).
+// PER_HEAD: one CTA per (request, head) instead (8 warps on one head's rows) when there are
+// fewer GQA groups than SMs but enough heads; the group is then planned by its last-decided
+// head (decide_head's arrival count).
+template <bool PER_HEAD>
 __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  const int grp = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
-  const int wph = 8 / g;                          // warps per head
-  const int hl = warp / wph, part = warp % wph;   // head in the group, share of its rows
-  const bool active = hl < g;
+  const int grp = PER_HEAD ? blockIdx.x / g : blockIdx.x;
+  const int wph = PER_HEAD ? 8 : 8 / g;           // warps per head
+  const int hl = PER_HEAD ? blockIdx.x % g : warp / wph, part = PER_HEAD ? warp : warp % wph;
+  const bool active = PER_HEAD || hl < g;
   const int b = grp / Hkv, kvh = grp % Hkv;
   const int bh = b * Hq + kvh * g + (active ? hl : 0);
   const int m = p.seq_lens[b] + 1;
@@ -317,7 +322,8 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   if (lane == 0) sD[warp] = dmin;
   __syncthreads();
   float D = CUDART_INF_F;
-  for (int w = hl * wph; w < hl * wph + wph && w < 8; ++w) D = fminf(D, sD[w]);
+  const int w0 = PER_HEAD ? 0 : hl * wph;
+  for (int w = w0; w < w0 + wph && w < 8; ++w) D = fminf(D, sD[w]);
   // 3. other rows of the share that can still beat D*: 8 lanes per row, up to 8 rows per
   //    lane group in flight (32 per warp per round; a fresh query makes every row survive)
   if (active && D != CUDART_INF_F) {
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   if (lane == 0) skey[warp] = key;
   __syncthreads();
   if (active && part == 0 && lane == 0) {
-    for (int w = hl * wph + 1; w < hl * wph + wph; ++w) key = skey[w] > key ? skey[w] : key;
+    for (int w = w0 + 1; w < w0 + wph; ++w) key = skey[w] > key ? skey[w] : key;
     double bd = CUDART_INF;
     int bpos = -1;
     if (key) {
@@ -371,8 +377,10 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
       bd = (double)__uint_as_float((unsigned)(raw >> 32));
       bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
     }
-    slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
+    if (PER_HEAD) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos);  // the group's last head plans it
+    else slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
   }
+  if (PER_HEAD) return;
   __syncthreads();
   if (tid == 0) {
     int lo_g = m;
@@ -382,9 +390,9 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
   }
 }
 
-cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st) {
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.batch * p.n_kv_heads);
+  cfg.gridDim = dim3(per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads);
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -392,7 +400,7 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, verify_kernel, p);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true>, p) : cudaLaunchKernelEx(&cfg, verify_kernel<false>, p);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -432,11 +440,12 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
     if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
   }
   const FrontVariant& v = kFrontVariants[vi];
-  // the two-pass front covers the match stage only: append-only launches use the one-pass kernel
-  // (verify_kernel gives each head 8/g warps: groups of up to 8 heads; with fewer groups than
-  // SMs, e.g. one long request, its one-CTA-per-group parallelism is too thin: one pass)
-  const bool two_pass = v.two_pass && do_match && p.n_q_heads / p.n_kv_heads <= 8 && p.batch * p.n_kv_heads >= 148 &&
-                        p.window <= 1024;
+  // the two-pass front covers the match stage only: append-only launches use the one-pass kernel,
+  // and so does a batch with fewer heads than SMs (one long request): too little verify parallelism
+  // verify: a CTA per GQA group when groups fill the SMs, a CTA per head when only heads do
+  const bool per_group = p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
+  const bool per_head = !per_group && p.batch * p.n_q_heads >= 148;
+  const bool two_pass = v.two_pass && do_match && (per_group || per_head) && p.window <= 1024;
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
@@ -446,7 +455,7 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
-  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st);
+  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st, per_head);
   return cudaSuccess;
 }
 

@@ -212,12 +212,14 @@ def test_step_graph_replay_equals_decode_step():
     assert graphed.seq_lens[0].tolist() == [L] * B
 
 
-def test_two_pass_match_large_batch_replay():
-    """Enough GQA groups (B * Hkv >= 148) for the two-pass match (first-half scan + verify):
-    decisions identical and outputs within tolerance of the oracle, hits and misses mixed."""
+@pytest.mark.parametrize("B,hq,hkv", [(37, 16, 4), (10, 16, 2)])
+def test_two_pass_match_large_batch_replay(B, hq, hkv):
+    """Enough heads for the two-pass match (first-half scan + verify): one verify CTA per GQA
+    group (B * Hkv >= 148) or per head (fewer groups, B * Hq >= 148); decisions identical
+    and outputs within tolerance of the oracle, hits and misses mixed."""
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
 
-    L, B, hq, hkv, W, r = 120, 37, 16, 4, 64, 16
+    L, W, r = 120, 64, 16
     trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=300 + s,
                                        rep_prob=0.7)) for s in range(B)]
     cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
