@@ -27,6 +27,11 @@
  *   mac_shard_partial / mac_shard_complete  decode_step split around the one
  *                     cross-GPU exchange of the KV-sharded path (all-gather of
  *                     per-shard (piece, band) summaries, then the merge)
+ *   mac_step_stats    DecodeMetrics.record_hit / record_miss (engine.py:188-205)
+ *                     and group_kv_span (engine.py:66-77, :525-528) accumulated
+ *                     on the device per head after a step
+ *   mac_mass_bound    mass_bound_check (engine.py:246-281), offline, over the
+ *                     paged cache
  *
  * Conventions: plain device pointers and sizes, no allocation inside, every
  * launch is stream-ordered and graph-capturable (no host synchronisation).
@@ -43,7 +48,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 2
+#define MACATTN_ABI_VERSION 3
 
 /* storage modes: dtype of the K/V cache and the query ring; summaries are
  * f32 in MAC_MODE_F32/BF16 and f64 in MAC_MODE_F64 (engine.py:152-153 allows
@@ -140,6 +145,39 @@ typedef struct MacMergeParams {
   void* out_lse;         /* [n_rows] */
 } MacMergeParams;
 
+/* Per-head decision statistics accumulated by mac_step_stats (f64 counters, summed
+ * over the batch): head_stats is [Hq, MAC_STAT_COUNT], group_stats [Hkv, MAC_GSTAT_COUNT].
+ * Fields follow DecodeMetrics (engine.py:167-186). */
+enum {
+  MAC_STAT_STEPS = 0,      /* decisions */
+  MAC_STAT_HITS = 1,       /* reuses taken (use_hit) */
+  MAC_STAT_FORCED = 2,     /* raw hits the gates turned into misses */
+  MAC_STAT_FALLBACKS = 3,  /* remove() fell back to the split prefix */
+  MAC_STAT_SKIP_SUM = 4,   /* sum of (p - r)+ / m over hits */
+  MAC_STAT_KV_READ = 5,    /* tokens read: m - (p - r)+ on a hit, m on a miss */
+  MAC_STAT_KV_FULL = 6,    /* tokens of full attention: m */
+  MAC_STAT_GAP_SUM = 7,    /* sum of m - p over hits */
+  MAC_STAT_RHO_SUM = 8,    /* sum of the band mass rho */
+  MAC_STAT_CANDIDATES = 9, /* ring rows scanned */
+  MAC_STAT_COUNT = 10
+};
+enum { MAC_GSTAT_KV_TOKENS = 0, MAC_GSTAT_KV_TOTAL = 1, MAC_GSTAT_COUNT = 2 };
+
+/* Items of mac_mass_bound: one hit each, keys / values [1, p] of (request, kv head)
+ * read from the paged cache described by the MacDecodeParams. */
+typedef struct MacMassBoundParams {
+  int32_t n_items;
+  int32_t band;                 /* r */
+  int32_t rotate;               /* 1: q_m / q_p are pre-RoPE, rotated at m / p in-kernel; 0: post-RoPE */
+  const int32_t* item_req;      /* [n] request (page_table row) */
+  const int32_t* item_kv_head;  /* [n] */
+  const int32_t* item_m;        /* [n] position of the current query */
+  const int32_t* item_p;        /* [n] hit position p >= 1 */
+  const double* q_m;            /* [n, d] current query */
+  const double* q_p;            /* [n, d] the ring query stored at p */
+  double* out;                  /* [n, 2] (lhs, rhs) of engine.py:246-281 */
+} MacMassBoundParams;
+
 int mac_abi_version(void);
 size_t mac_params_size(void);
 const char* mac_error_string(int code);
@@ -175,6 +213,13 @@ int mac_shard_complete(const MacDecodeParams* p, void* stream);
  * in-kernel, then seq_lens += n_tokens.  No ring work (the reference fills rings one
  * decode step at a time, engine.py:374-402; see BatchDecodeEngine.prefill). */
 int mac_prefill_kv(const MacDecodeParams* p, int32_t n_tokens, void* stream);
+/* after a decode step: add its per-head decisions (match_hit, use_hit, match_pos,
+ * match_scanned, band_mass, fallbacks, seq_lens = m) into head_stats / group_stats.
+ * Only the fields listed are read; the step's other buffers may be NULL. */
+int mac_step_stats(const MacDecodeParams* p, double* head_stats, double* group_stats, void* stream);
+/* mass_bound_check for n_items hits; p supplies the cache geometry (storage, dims,
+ * page_table, k_cache, v_cache, rope_freqs); d, d_v <= 256; no KV sharding. */
+int mac_mass_bound(const MacDecodeParams* p, const MacMassBoundParams* mb, void* stream);
 
 #ifdef __cplusplus
 }

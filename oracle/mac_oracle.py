@@ -17,6 +17,7 @@ It is a numpy restatement of the reference package `attnreuse`
 * ring write-back        engine.py:374-402    (rectify_append)
 * metrics                engine.py:167-243    (DecodeMetrics, compute_metrics)
 * batched oracle         engine.py:542-572    (oracle_outputs)
+* prefix mass bound      engine.py:246-281    (mass_bound_check)
 
 One extension beyond the reference: storage "bf16" (keys, values and ring
 queries rounded through bfloat16, summaries through float32), the storage
@@ -51,6 +52,7 @@ __all__ = [
     "OracleStep",
     "oracle_outputs",
     "metrics_report",
+    "mass_bound_check",
 ]
 
 EMPTY_LSE = -math.inf
@@ -530,6 +532,35 @@ class OracleEngine:
             mt.group_kv_tokens += m - floor
             mt.group_kv_total += m
         return OracleStep(out, hit, use, ps, dist, scanned, flse, pacc, plse, rho_all)
+
+
+def mass_bound_check(q_m, q_p, keys, values, band: int) -> tuple[float, float]:
+    """Drift of the reused non-band prefix vs its first-order bound (engine.py:246-281).
+
+    Softmaxes of both post-RoPE queries over keys [1, p]; cut = (p - band)+;
+    lhs = ||sum_{t<=cut} (a_p - a_m)_t v_t||, rhs = expm1(max_{t<=cut}|l_m - l_p|)
+    * (1 - rho) * E_{a_p}[||v||] over the prefix, rho = a_p's band share."""
+    keys = np.asarray(keys, dtype=np.float64)
+    values = np.asarray(values, dtype=np.float64)
+    n = keys.shape[0]
+    if n < 1:
+        raise ValueError("mass_bound_check needs at least one token")
+    sc = 1.0 / math.sqrt(keys.shape[1])
+    lp = keys @ np.asarray(q_p, dtype=np.float64) * sc
+    lm = keys @ np.asarray(q_m, dtype=np.float64) * sc
+    wp = np.exp(lp - lp.max())
+    wm = np.exp(lm - lm.max())
+    zp, zm = wp.sum(), wm.sum()
+    cut = max(0, n - band)
+    if cut == 0:
+        return 0.0, 0.0
+    rho = float(wp[cut:].sum() / zp)
+    drift = (wp[:cut] / zp - wm[:cut] / zm) @ values[:cut]
+    lhs = float(np.sqrt(drift @ drift))
+    dl = float(np.max(np.abs(lm[:cut] - lp[:cut])))
+    pre = float(wp[:cut].sum())
+    ev = float(wp[:cut] @ np.sqrt((values[:cut] ** 2).sum(axis=1))) / pre if pre > 0 else 0.0
+    return lhs, math.expm1(dl) * (1.0 - rho) * ev
 
 
 def oracle_outputs(q_pre, k_pre, v, cfg: OracleConfig, chunk: int = 256) -> np.ndarray:

@@ -40,7 +40,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the device engines import torch; load them on first use
     if name in ("BatchDecodeEngine", "BatchStepResult", "DecodeEngine", "StepGraph", "run_decode", "KvStoreView",
-                "QueryRingView", "SummaryRingView", "TrafficCounter", "rope_freqs"):
+                "QueryRingView", "SummaryRingView", "TrafficCounter", "rope_freqs", "mass_bound_check"):
         from . import engine
 
         return getattr(engine, name)
@@ -53,5 +53,5 @@ __all__ = [
     "MATCH_POST_ROPE", "MATCH_PRE_ROPE", "MassExceededError", "MatchConfig", "MatchResult", "PRESETS",
     "StepGraph", "StepResult", "SyntheticSpec", "Trace", "TraceError", "TrafficCounter", "aux_overhead_ratio",
     "aux_overhead_rule_of_thumb", "break_even_gate", "compute_metrics", "empty_summary", "fidelity_efficiency",
-    "finalize", "gen_synthetic", "group_kv_span", "read_trace", "run_decode", "threshold", "write_trace",
+    "finalize", "gen_synthetic", "group_kv_span", "mass_bound_check", "read_trace", "run_decode", "threshold", "write_trace",
 ]

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
@@ -39,7 +39,14 @@ EXPORTS = (
     "mac_shard_partial",
     "mac_shard_complete",
     "mac_prefill_kv",
+    "mac_step_stats",
+    "mac_mass_bound",
 )
+
+# per-head / per-group statistics fields of mac_step_stats (include/macattn.h)
+STAT_FIELDS = ("steps", "hits", "forced_misses", "fallbacks", "skip_sum", "kv_tokens_read",
+               "kv_tokens_full", "gap_sum", "band_mass_sum", "match_candidates")
+GSTAT_FIELDS = ("group_kv_tokens", "group_kv_total")
 
 
 class MacDecodeParams(C.Structure):
@@ -112,6 +119,21 @@ class MacMergeParams(C.Structure):
     ]
 
 
+class MacMassBoundParams(C.Structure):
+    _fields_ = [
+        ("n_items", C.c_int32),
+        ("band", C.c_int32),
+        ("rotate", C.c_int32),
+        ("item_req", C.c_void_p),
+        ("item_kv_head", C.c_void_p),
+        ("item_m", C.c_void_p),
+        ("item_p", C.c_void_p),
+        ("q_m", C.c_void_p),
+        ("q_p", C.c_void_p),
+        ("out", C.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -144,6 +166,10 @@ def load() -> C.CDLL:
         fn.argtypes = [C.POINTER(MacDecodeParams), C.c_void_p]
     lib.mac_prefill_kv.restype = C.c_int
     lib.mac_prefill_kv.argtypes = [C.POINTER(MacDecodeParams), C.c_int32, C.c_void_p]
+    lib.mac_step_stats.restype = C.c_int
+    lib.mac_step_stats.argtypes = [C.POINTER(MacDecodeParams), C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.mac_mass_bound.restype = C.c_int
+    lib.mac_mass_bound.argtypes = [C.POINTER(MacDecodeParams), C.POINTER(MacMassBoundParams), C.c_void_p]
     lib.mac_merge_partials.restype = C.c_int
     lib.mac_merge_partials.argtypes = [C.POINTER(MacMergeParams), C.c_void_p]
     if lib.mac_abi_version() != ABI_VERSION:

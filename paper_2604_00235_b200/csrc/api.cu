@@ -18,6 +18,8 @@ bool match_fast_supported(const MacDecodeParams&);
 bool front_fast_supported(const MacDecodeParams&);
 cudaError_t launch_merge_partials(const MacMergeParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_prefill_kv(const MacDecodeParams&, int, cudaStream_t);
+template <int MODE> cudaError_t launch_step_stats(const MacDecodeParams&, double*, double*, cudaStream_t);
+template <int MODE> cudaError_t launch_mass_bound(const MacDecodeParams&, const MacMassBoundParams&, cudaStream_t);
 }  // namespace mac
 
 using namespace mac;
@@ -178,6 +180,40 @@ int mac_prefill_kv(const MacDecodeParams* p, int32_t n_tokens, void* stream) {
     case MAC_MODE_F32: return (int)launch_prefill_kv<MAC_MODE_F32>(*p, n_tokens, st);
     case MAC_MODE_BF16: return (int)launch_prefill_kv<MAC_MODE_BF16>(*p, n_tokens, st);
     default: return (int)launch_prefill_kv<MAC_MODE_F64>(*p, n_tokens, st);
+  }
+}
+
+int mac_step_stats(const MacDecodeParams* p, double* head_stats, double* group_stats, void* stream) {
+  if (!p || !head_stats || !group_stats) return MAC_ERR_NULL;
+  if (p->batch < 1 || p->n_q_heads < 1 || p->n_kv_heads < 1 || p->n_q_heads % p->n_kv_heads || p->band < 0)
+    return MAC_ERR_SHAPE;
+  if (p->storage < MAC_MODE_F32 || p->storage > MAC_MODE_F64) return MAC_ERR_DTYPE;
+  if (!p->seq_lens || !p->match_hit || !p->use_hit || !p->match_pos || !p->match_scanned || !p->band_mass)
+    return MAC_ERR_NULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (p->storage) {
+    case MAC_MODE_F32: return (int)launch_step_stats<MAC_MODE_F32>(*p, head_stats, group_stats, st);
+    case MAC_MODE_BF16: return (int)launch_step_stats<MAC_MODE_BF16>(*p, head_stats, group_stats, st);
+    default: return (int)launch_step_stats<MAC_MODE_F64>(*p, head_stats, group_stats, st);
+  }
+}
+
+int mac_mass_bound(const MacDecodeParams* p, const MacMassBoundParams* mb, void* stream) {
+  if (!p || !mb) return MAC_ERR_NULL;
+  if (p->n_kv_heads < 1 || p->head_dim < 1 || (mb->rotate && p->head_dim % 2) || p->head_dim > 256 || p->head_dim_v < 1 ||
+      p->head_dim_v > 256 || mb->band < 0 || mb->n_items < 0 || p->kv_offset != 0)
+    return MAC_ERR_SHAPE;
+  if (p->storage < MAC_MODE_F32 || p->storage > MAC_MODE_F64) return MAC_ERR_DTYPE;
+  if (p->page_size < 1 || p->pages_per_seq < 1) return MAC_ERR_PAGING;
+  if (!p->page_table || !p->k_cache || !p->v_cache || (mb->rotate && !p->rope_freqs)) return MAC_ERR_NULL;
+  if (mb->n_items == 0) return MAC_OK;
+  if (!mb->item_req || !mb->item_kv_head || !mb->item_m || !mb->item_p || !mb->q_m || !mb->q_p || !mb->out)
+    return MAC_ERR_NULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (p->storage) {
+    case MAC_MODE_F32: return (int)launch_mass_bound<MAC_MODE_F32>(*p, *mb, st);
+    case MAC_MODE_BF16: return (int)launch_mass_bound<MAC_MODE_BF16>(*p, *mb, st);
+    default: return (int)launch_mass_bound<MAC_MODE_F64>(*p, *mb, st);
   }
 }
 

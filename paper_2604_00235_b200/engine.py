@@ -47,6 +47,49 @@ _IN_DT = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16, torch.float6
 SM_COUNT_B200 = 148
 
 
+def C_void(ptr: int):
+    import ctypes
+
+    return ctypes.c_void_p(ptr)
+
+
+def mass_bound_check(q_m, q_p, keys, values, band: int, *, device="cuda") -> tuple[float, float]:
+    """Reference signature of mass_bound_check (engine.py:246-281): post-RoPE queries q_m, q_p (d,),
+    keys [p, d] and values [p, d_v] covering [1, p]; returns (lhs, rhs).  Runs the fp64 CUDA kernel
+    (mac_mass_bound) over the arrays laid out as one KV page."""
+    keys = np.asarray(keys, dtype=np.float64)
+    values = np.asarray(values, dtype=np.float64)
+    if keys.ndim != 2 or values.ndim != 2 or values.shape[0] != keys.shape[0]:
+        raise ValueError("keys and values must be [p, d] and [p, d_v]")
+    n, d = keys.shape
+    if n < 1:
+        raise ValueError("mass_bound_check needs at least one token")
+    dv = values.shape[1]
+    lib = _lib.load()
+    dev = torch.device(device)
+    kc = torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
+    vc = torch.from_numpy(np.ascontiguousarray(values)).to(dev)
+    qs = torch.from_numpy(np.stack([np.asarray(q_m, dtype=np.float64), np.asarray(q_p, dtype=np.float64)])).to(dev)
+    zeros = torch.zeros(4, dtype=torch.int32, device=dev)
+    item_pm = torch.tensor([n], dtype=torch.int32, device=dev)
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    P = _lib.MacDecodeParams()
+    P.batch = P.n_q_heads = P.n_kv_heads = 1
+    P.head_dim, P.head_dim_v = d, dv
+    P.page_size, P.pages_per_seq = n, 1
+    P.storage = _lib.MODE_F64
+    P.page_table = zeros.data_ptr()
+    P.k_cache, P.v_cache = kc.data_ptr(), vc.data_ptr()
+    mb = _lib.MacMassBoundParams()
+    mb.n_items, mb.band, mb.rotate = 1, int(band), 0
+    mb.item_req = mb.item_kv_head = zeros.data_ptr()
+    mb.item_m = mb.item_p = item_pm.data_ptr()
+    mb.q_m, mb.q_p, mb.out = qs[0].data_ptr(), qs[1].data_ptr(), out.data_ptr()
+    _lib.check(lib.mac_mass_bound(P, mb, torch.cuda.current_stream(dev).cuda_stream), "mac_mass_bound")
+    lhs, rhs = out.cpu().tolist()
+    return float(lhs), float(rhs)
+
+
 def rope_freqs(d: int, base: float) -> np.ndarray:
     """omega_j = base**(-2j/d) evaluated exactly as attention.py:208-209 (numpy f64)."""
     j = np.arange(d // 2, dtype=np.float64)
@@ -85,7 +128,8 @@ class BatchDecodeEngine:
 
     def __init__(self, cfg: EngineConfig, batch: int, max_seq_len: int, *, device="cuda",
                  max_chunks: int | None = None, min_chunk: int = 128, page_perm_seed: int | None = None,
-                 record_cached: bool = False, kv_offset: int = 0, kv_limit: int = 0, n_shards: int = 0):
+                 record_cached: bool = False, kv_offset: int = 0, kv_limit: int = 0, n_shards: int = 0,
+                 track_stats: bool = False):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         if max_seq_len < 1:
@@ -137,6 +181,10 @@ class BatchDecodeEngine:
         self.shard_send = torch.zeros(B, Hq, 2, dv + 1, dtype=self.sumdt, device=dev) if n_shards else None
         self.shard_parts = (torch.zeros(n_shards, B, Hq, 2, dv + 1, dtype=self.sumdt, device=dev)
                             if n_shards else None)
+        # device-side decision statistics per (layer, head) (mac_step_stats)
+        self.track_stats = track_stats
+        self.head_stats = torch.zeros(L, Hq, len(_lib.STAT_FIELDS), dtype=torch.float64, device=dev)
+        self.group_stats = torch.zeros(L, cfg.n_kv_heads, len(_lib.GSTAT_FIELDS), dtype=torch.float64, device=dev)
         probe = self._params(0, self.o_out, self.o_out, self.o_out, _lib.DT_F32)
         # zeroed once: the match kernel keeps its cross-CTA keys/counters zero between steps
         self.workspace = torch.zeros(int(_lib.load().mac_workspace_bytes(probe)), dtype=torch.uint8, device=dev)
@@ -269,8 +317,87 @@ class BatchDecodeEngine:
         refresh gate does (engine.py:456-459)."""
         self._layer(layer)
         dt = self._check_inputs(q_pre, k_pre, v)
-        _lib.call("mac_decode_step", self._params(layer, q_pre, k_pre, v, dt, force_miss), self._stream())
+        P = self._params(layer, q_pre, k_pre, v, dt, force_miss)
+        _lib.call("mac_decode_step", P, self._stream())
+        if self.track_stats and not getattr(self, "_in_prefill", False):
+            self._accumulate_stats(layer, P)
         return self.result()
+
+    # ------------------------------------------------------------------ diagnostics
+    def _accumulate_stats(self, layer: int, P):
+        code = _lib.load().mac_step_stats(P, C_void(self.head_stats[layer].data_ptr()),
+                                          C_void(self.group_stats[layer].data_ptr()), self._stream())
+        _lib.check(code, "mac_step_stats")
+
+    def reset_stats(self):
+        self.head_stats.zero_()
+        self.group_stats.zero_()
+
+    def stats(self, layer: int | None = None, *, per_head: bool = False) -> dict:
+        """Decision statistics accumulated on the device since the last reset (track_stats=True),
+        in the reference's report schema (compute_metrics, engine.py:226-243) plus the raw
+        DecodeMetrics counters; `layer=None` sums every layer.  per_head adds per-head arrays of
+        acceptance, skip ratio, kv fraction and mean band mass (one host copy, on request)."""
+        hs = (self.head_stats.sum(0) if layer is None else self.head_stats[layer]).cpu().numpy()
+        gs = (self.group_stats.sum(0) if layer is None else self.group_stats[layer]).cpu().numpy()
+        f = {name: hs[:, i] for i, name in enumerate(_lib.STAT_FIELDS)}
+        tot = {name: float(v.sum()) for name, v in f.items()}
+        steps = tot["steps"]
+        rep = {
+            "schema_version": 1,
+            "steps": int(steps),
+            "hits": int(tot["hits"]),
+            "acceptance_rate": tot["hits"] / steps if steps else None,
+            "skip_ratio": tot["skip_sum"] / steps if steps else None,
+            "kv_fraction": tot["kv_tokens_read"] / tot["kv_tokens_full"] if tot["kv_tokens_full"] else None,
+            "err_mean": None, "err_p50": None, "err_p99": None,
+            "mean_gap": tot["gap_sum"] / tot["hits"] if tot["hits"] else None,
+            "mean_band_mass": tot["band_mass_sum"] / steps if steps else None,
+            "forced_misses": int(tot["forced_misses"]),
+            "fallbacks": int(tot["fallbacks"]),
+            "kv_tokens_read": int(tot["kv_tokens_read"]),
+            "kv_tokens_full": int(tot["kv_tokens_full"]),
+            "match_candidates": int(tot["match_candidates"]),
+            "group_kv_tokens": int(gs[:, 0].sum()),
+            "group_kv_total": int(gs[:, 1].sum()),
+        }
+        if per_head:
+            with np.errstate(invalid="ignore", divide="ignore"):
+                rep["per_head"] = {
+                    "steps": f["steps"].astype(np.int64),
+                    "acceptance_rate": f["hits"] / f["steps"],
+                    "skip_ratio": f["skip_sum"] / f["steps"],
+                    "kv_fraction": f["kv_tokens_read"] / f["kv_tokens_full"],
+                    "mean_band_mass": f["band_mass_sum"] / f["steps"],
+                    "mean_gap": f["gap_sum"] / f["hits"],
+                }
+                rep["per_group_kv_fraction"] = gs[:, 0] / gs[:, 1]
+        return rep
+
+    def mass_bound(self, layer: int, req, kv_head, m, p, q_m: torch.Tensor, q_p: torch.Tensor) -> torch.Tensor:
+        """mass_bound_check (engine.py:246-281) for n hits over this layer's paged cache: keys and
+        values [1, p] of (req, kv_head), pre-RoPE queries q_m (rotated at m) and q_p (the ring query
+        stored at p, rotated at p), [n, d] float64.  Returns [n, 2] float64 (lhs, rhs) on the device."""
+        self._layer(layer)
+        cfg, dev = self.cfg, self.device
+        i32 = lambda x: torch.as_tensor(x, dtype=torch.int32).reshape(-1).to(dev)
+        req, kvh, mm, pp = i32(req), i32(kv_head), i32(m), i32(p)
+        n = req.numel()
+        if not (kvh.numel() == mm.numel() == pp.numel() == n):
+            raise ValueError("req, kv_head, m and p must have the same length")
+        if n and int(pp.min().item()) < 1:
+            raise ValueError("mass_bound_check needs at least one token")
+        qm = q_m.to(device=dev, dtype=torch.float64).reshape(n, cfg.d).contiguous()
+        qp = q_p.to(device=dev, dtype=torch.float64).reshape(n, cfg.d).contiguous()
+        out = torch.zeros(n, 2, dtype=torch.float64, device=dev)
+        P = self._params(layer, self.o_out, self.o_out, self.o_out, _lib.DT_F32)
+        mb = _lib.MacMassBoundParams()
+        mb.n_items, mb.band, mb.rotate = n, cfg.band, 1
+        mb.item_req, mb.item_kv_head, mb.item_m, mb.item_p = (req.data_ptr(), kvh.data_ptr(), mm.data_ptr(),
+                                                              pp.data_ptr())
+        mb.q_m, mb.q_p, mb.out = qm.data_ptr(), qp.data_ptr(), out.data_ptr()
+        _lib.check(_lib.load().mac_mass_bound(P, mb, self._stream()), "mac_mass_bound")
+        return out
 
     def prefill(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor) -> BatchStepResult | None:
         """Append a prompt of n tokens to every request ([B, n, H, d] tensors, token-major) and
@@ -298,9 +425,13 @@ class BatchDecodeEngine:
             code = _lib.load().mac_prefill_kv(P, n_bulk, self._stream())
             _lib.check(code, "mac_prefill_kv")
         res = None
-        for t in range(n_bulk, n):
-            res = self.decode_step(layer, q_pre[:, t].contiguous(), k_pre[:, t].contiguous(), v[:, t].contiguous(),
-                                   force_miss=True)
+        self._in_prefill = True  # prompt tokens are not decode decisions: no statistics
+        try:
+            for t in range(n_bulk, n):
+                res = self.decode_step(layer, q_pre[:, t].contiguous(), k_pre[:, t].contiguous(),
+                                       v[:, t].contiguous(), force_miss=True)
+        finally:
+            self._in_prefill = False
         return res
 
     def stage(self, name: str, layer: int, q_pre, k_pre, v, force_miss: bool = False):
@@ -566,6 +697,9 @@ class DecodeEngine:
         q = torch.from_numpy(q_pre).to(dev)[None].contiguous()
         k = torch.from_numpy(k_pre).to(dev)[None].contiguous()
         vv = torch.from_numpy(v).to(dev)[None].contiguous()
+        mass_check = cfg.mass_check and cfg.oracle_mode
+        if mass_check:  # the step overwrites ring slot (m-1) % W, which may hold q at p = m - W
+            ring_prev = self.batch.ring_q[layer][0, :, (m - 1) % cfg.window].clone()
         res = self.batch.decode_step(layer, q, k, vv)
         host = {name: t[0].cpu().numpy() for name, t in (
             ("out", res.out), ("hit", res.match_hit), ("use", res.use_hit), ("pos", res.match_pos),
@@ -583,6 +717,18 @@ class DecodeEngine:
                         self.oracle_traffic.record(m, m * self.store.token_bytes)
 
         delta = DecodeMetrics()
+        if mass_check and host["use"].any():
+            # engine.py:480-483: per hit, q_m at m and the ring query at p, keys [1, p]
+            hs = [h for h in range(cfg.n_q_heads) if host["use"][h]]
+            ps = [int(host["pos"][h]) for h in hs]
+            ring = self.batch.ring_q[layer][0]
+            q_p = torch.stack([ring_prev[h] if p == m - cfg.window else ring[h, (p - 1) % cfg.window]
+                               for h, p in zip(hs, ps)]).double()
+            mb = self.batch.mass_bound(layer, [0] * len(hs), [h // self._group for h in hs], [m] * len(hs), ps,
+                                       q[0, hs], q_p).cpu().numpy()
+            delta.mass_bound_samples.extend((float(a), float(b)) for a, b in mb)
+            for p in ps:
+                self.oracle_traffic.record(p, p * self.store.token_bytes)
         outputs = host["out"].astype(np.float64)
         matches, fulls, cacheds, masses = [], [], [], []
         errs = [] if cfg.oracle_mode else None

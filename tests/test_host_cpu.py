@@ -143,3 +143,38 @@ def test_library_rejects_bad_params_without_gpu():
     assert lib.mac_decode_step(p, None) == 1001  # null pointers
     p.storage = 7
     assert lib.mac_decode_step(p, None) == 1003
+
+
+def test_stat_fields_follow_the_header():
+    from paper_2604_00235_b200 import _lib
+
+    with open(os.path.join(ROOT, "include", "macattn.h")) as fh:
+        src = fh.read()
+    stat = dict((k, int(v)) for k, v in re.findall(r"MAC_STAT_(\w+)\s*=\s*(\d+)", src))
+    gstat = dict((k, int(v)) for k, v in re.findall(r"MAC_GSTAT_(\w+)\s*=\s*(\d+)", src))
+    assert stat.pop("COUNT") == len(_lib.STAT_FIELDS) and sorted(stat.values()) == list(range(len(stat)))
+    assert gstat.pop("COUNT") == len(_lib.GSTAT_FIELDS)
+    names = {"STEPS": "steps", "HITS": "hits", "FORCED": "forced_misses", "FALLBACKS": "fallbacks",
+             "SKIP_SUM": "skip_sum", "KV_READ": "kv_tokens_read", "KV_FULL": "kv_tokens_full",
+             "GAP_SUM": "gap_sum", "RHO_SUM": "band_mass_sum", "CANDIDATES": "match_candidates"}
+    for k, i in stat.items():
+        assert _lib.STAT_FIELDS[i] == names[k]
+
+
+def test_diagnostic_entry_points_validate_without_gpu():
+    import ctypes
+
+    from paper_2604_00235_b200 import _lib
+
+    lib = _lib.load()
+    p = _lib.MacDecodeParams()
+    assert lib.mac_step_stats(p, None, None, None) == 1001
+    buf = (ctypes.c_double * 64)()
+    assert lib.mac_step_stats(p, buf, buf, None) == 1002  # zero batch
+    p.batch, p.n_q_heads, p.n_kv_heads = 1, 4, 2
+    assert lib.mac_step_stats(p, buf, buf, None) == 1001  # decision buffers missing
+    mb = _lib.MacMassBoundParams()
+    p.head_dim, p.head_dim_v, p.page_size, p.pages_per_seq = 8, 8, 16, 1
+    assert lib.mac_mass_bound(p, mb, None) == 1001  # no cache
+    p.head_dim = 512
+    assert lib.mac_mass_bound(p, mb, None) == 1002  # d > 256

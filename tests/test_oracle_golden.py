@@ -102,3 +102,16 @@ def test_bf16_rounding_is_rne():
 
     want = torch.from_numpy(x).bfloat16().double().numpy()
     np.testing.assert_array_equal(got, want)
+
+
+def test_oracle_mass_bound_matches_reference():
+    """mass_bound_check (engine.py:246-281) restated; pinned on the reference's outputs."""
+    from mac_oracle import mass_bound_check
+
+    z = load("mass_bound")
+    for i in range(int(z["n_cases"])):
+        got = mass_bound_check(z[f"c{i}__q_m"], z[f"c{i}__q_p"], z[f"c{i}__keys"], z[f"c{i}__values"],
+                               int(z[f"c{i}__band"]))
+        np.testing.assert_allclose(got, z[f"c{i}__out"], rtol=1e-12, atol=1e-16, err_msg=f"case {i}")
+    samples = z["run_samples"]
+    assert samples.shape[1] == 2 and (samples >= 0).all()
