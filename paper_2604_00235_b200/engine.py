@@ -491,33 +491,57 @@ class BatchDecodeEngine:
 
 
 class StepGraph:
-    """One decode step of a BatchDecodeEngine layer as a replayable CUDA graph, with the
-    step's host I/O inside it: pinned host inputs -> device, the step's kernels, output ->
-    pinned host.  The serving loop writes a step's q/k/v into `q_host`/`k_host`/`v_host`,
-    calls `replay()`, and reads `out_host` after the stream syncs.  Replays are
-    stream-ordered and advance the engine like `decode_step` (every kernel reads its
-    position from `seq_lens`, every workspace counter returns to zero by the end of the
-    step), so one graph serves every step of the layer."""
+    """One decode step of a BatchDecodeEngine as a replayable CUDA graph, with the step's host
+    I/O inside it: pinned host inputs -> device, the step's kernels, output -> pinned host.
+    The serving loop writes a step's q/k/v into `q_host`/`k_host`/`v_host`, calls `replay()`,
+    and reads `out_host` after the stream syncs.  Replays are stream-ordered and advance the
+    engine like `decode_step` (every kernel reads its position from `seq_lens`, every
+    workspace counter returns to zero by the end of the step), so one graph serves every step.
 
-    def __init__(self, eng: "BatchDecodeEngine", layer: int, dtype=torch.bfloat16, out_dtype=None):
+    `layer` is one layer index, or a sequence of layers captured back to back in one graph
+    (one token of a trace replay across the model: one H2D copy of every
+    layer's q/k/v, one launch of the graph, one D2H copy of every layer's output); the host
+    buffers then carry a leading layer dimension in the order given."""
+
+    def __init__(self, eng: "BatchDecodeEngine", layer, dtype=torch.bfloat16, out_dtype=None):
         """dtype: the q/k/v input dtype; out_dtype: the host output dtype (default the engine's
         summary dtype, f32 for bf16 storage; bf16 halves the device-to-host bytes)."""
         cfg, B = eng.cfg, eng.batch
-        eng._layer(layer)
-        self.eng, self.layer = eng, layer
+        self.multi = not isinstance(layer, int)
+        self.layers = [int(x) for x in layer] if self.multi else [int(layer)]
+        if not self.layers or len(set(self.layers)) != len(self.layers):
+            raise ValueError("layers must be a non-empty sequence of distinct layer indices")
+        for lay in self.layers:
+            eng._layer(lay)
+        self.eng, self.layer = eng, (self.layers if self.multi else self.layers[0])
+        n_l = len(self.layers)
         dev = eng.device
-        # q, k and v share one pinned staging buffer and one device buffer: one H2D copy per step
+        # q, k and v of every layer share one pinned staging buffer and one device buffer:
+        # one H2D copy per step
         nq, nk, nv = B * cfg.n_q_heads * cfg.d, B * cfg.n_kv_heads * cfg.d, B * cfg.n_kv_heads * cfg.d_v
-        self.in_host = torch.zeros(nq + nk + nv, dtype=dtype).pin_memory()
-        self.in_dev = torch.zeros(nq + nk + nv, dtype=dtype, device=dev)
-        split = lambda t: (t[:nq].view(B, cfg.n_q_heads, cfg.d), t[nq:nq + nk].view(B, cfg.n_kv_heads, cfg.d),  # noqa: E731
-                           t[nq + nk:].view(B, cfg.n_kv_heads, cfg.d_v))
+        per = nq + nk + nv
+        self.in_host = torch.zeros(n_l * per, dtype=dtype).pin_memory()
+        self.in_dev = torch.zeros(n_l * per, dtype=dtype, device=dev)
+
+        def split(t):
+            v = t.view(n_l, per)
+            q = v[:, :nq].view(n_l, B, cfg.n_q_heads, cfg.d)
+            k = v[:, nq:nq + nk].view(n_l, B, cfg.n_kv_heads, cfg.d)
+            vv = v[:, nq + nk:].view(n_l, B, cfg.n_kv_heads, cfg.d_v)
+            return (q, k, vv) if self.multi else (q[0], k[0], vv[0])
+
         self.q_host, self.k_host, self.v_host = split(self.in_host)
-        self.q_dev, self.k_dev, self.v_dev = split(self.in_dev)
+        self._qkv_dev = [(self.in_dev[i * per:i * per + nq].view(B, cfg.n_q_heads, cfg.d),
+                          self.in_dev[i * per + nq:i * per + nq + nk].view(B, cfg.n_kv_heads, cfg.d),
+                          self.in_dev[i * per + nq + nk:(i + 1) * per].view(B, cfg.n_kv_heads, cfg.d_v))
+                         for i in range(n_l)]
+        self.q_dev, self.k_dev, self.v_dev = self._qkv_dev[0]
         self.out_dtype = out_dtype or eng.sumdt
-        self.out_host = torch.zeros(B, cfg.n_q_heads, cfg.d_v, dtype=self.out_dtype).pin_memory()
-        self.out_dev = (torch.zeros(B, cfg.n_q_heads, cfg.d_v, dtype=self.out_dtype, device=dev)
-                        if self.out_dtype != eng.sumdt else None)
+        oshape = (n_l, B, cfg.n_q_heads, cfg.d_v) if self.multi else (B, cfg.n_q_heads, cfg.d_v)
+        self.out_host = torch.zeros(oshape, dtype=self.out_dtype).pin_memory()
+        # a device staging output when the dtype narrows or several layers share the engine's o_out
+        self.out_dev = (torch.zeros(oshape, dtype=self.out_dtype, device=dev)
+                        if (self.out_dtype != eng.sumdt or self.multi) else None)
         self.graph = torch.cuda.CUDAGraph()
         self.h2d_bytes = self.in_host.numel() * self.in_host.element_size()
         self.d2h_bytes = self.out_host.numel() * self.out_host.element_size()
@@ -531,12 +555,12 @@ class StepGraph:
     def _body(self):
         eng = self.eng
         self.in_dev.copy_(self.in_host, non_blocking=True)
-        eng.decode_step(self.layer, self.q_dev, self.k_dev, self.v_dev)
-        if self.out_dev is not None:  # narrowed on the device first: fewer bytes over the host link
-            self.out_dev.copy_(eng.o_out)
-            self.out_host.copy_(self.out_dev, non_blocking=True)
-        else:
-            self.out_host.copy_(eng.o_out, non_blocking=True)
+        for i, lay in enumerate(self.layers):
+            q, k, v = self._qkv_dev[i]
+            eng.decode_step(lay, q, k, v)
+            if self.out_dev is not None:  # narrowed on the device first: fewer bytes over the host link
+                (self.out_dev[i] if self.multi else self.out_dev).copy_(eng.o_out)
+        self.out_host.copy_(self.out_dev if self.out_dev is not None else eng.o_out, non_blocking=True)
 
     def replay(self):
         self.graph.replay()

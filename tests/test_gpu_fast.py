@@ -212,6 +212,48 @@ def test_step_graph_replay_equals_decode_step():
     assert graphed.seq_lens[0].tolist() == [L] * B
 
 
+def test_step_graph_across_layers():
+    """One graph for one token across every layer: identical to per-layer
+    decode_step calls, including device-side stats captured inside the graph."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, StepGraph, SyntheticSpec, gen_synthetic
+
+    L, B, hq, hkv, nl = 120, 3, 8, 2, 3
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_layers=nl, n_q_heads=hq, n_kv_heads=hkv,
+                                       seed=90 + s)) for s in range(B)]
+    q = torch.from_numpy(np.stack([bf16_round(t.q_pre) for t in trs], 2)).bfloat16()  # [L, nl, B, H, d]
+    k = torch.from_numpy(np.stack([bf16_round(t.k_pre) for t in trs], 2)).bfloat16()
+    v = torch.from_numpy(np.stack([bf16_round(t.v) for t in trs], 2)).bfloat16()
+    cfg = EngineConfig(d=128, d_v=128, n_layers=nl, n_q_heads=hq, n_kv_heads=hkv, window=32, band=8,
+                       storage="bf16", tau_per_layer=(0.3, 0.45, 0.6))
+    direct = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32, track_stats=True)
+    graphed = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32, track_stats=True)
+    order = [2, 0, 1]  # any order of distinct layers
+    sg = StepGraph(graphed, order, out_dtype=torch.bfloat16)
+    assert tuple(sg.q_host.shape) == (nl, B, hq, 128) and tuple(sg.out_host.shape) == (nl, B, hq, 128)
+    for m in range(1, L + 1):
+        want = []
+        for lay in order:
+            res = direct.decode_step(lay, q[m - 1, lay].cuda(), k[m - 1, lay].cuda(), v[m - 1, lay].cuda())
+            want.append(res.out.cpu().bfloat16())
+        for i, lay in enumerate(order):
+            sg.q_host[i].copy_(q[m - 1, lay])
+            sg.k_host[i].copy_(k[m - 1, lay])
+            sg.v_host[i].copy_(v[m - 1, lay])
+        sg.replay()
+        torch.cuda.synchronize()
+        for i in range(nl):
+            assert torch.equal(sg.out_host[i], want[i]), (m, i)
+    for lay in range(nl):
+        assert torch.equal(graphed.ring_acc[lay], direct.ring_acc[lay])
+        assert graphed.seq_lens[lay].tolist() == [L] * B
+        gs, ds = graphed.stats(lay), direct.stats(lay)
+        for key, val in ds.items():  # atomics add in any order: float sums agree to rounding
+            assert gs[key] == (pytest.approx(val, rel=1e-12) if isinstance(val, float) else val), key
+    assert direct.stats()["hits"] > 0
+    with pytest.raises(ValueError):
+        StepGraph(graphed, [0, 0])
+
+
 @pytest.mark.parametrize("B,hq,hkv", [(37, 16, 4), (10, 16, 2)])
 def test_two_pass_match_large_batch_replay(B, hq, hkv):
     """Enough heads for the two-pass match (first-half scan + verify): one verify CTA per GQA
