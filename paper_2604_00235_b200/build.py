@@ -21,12 +21,16 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "lib", "libmacattn.so")
+# MAC_TIMELINE=1 builds a development variant (lib/libmacattn_tl.so) whose kernels stamp
+# %globaltimer at entry / after the grid-dependency wait / exit into the workspace
+# (tools/timeline.py reads it); the product library is never built with it.
+TIMELINE = os.environ.get("MAC_TIMELINE") == "1"
+OBJ = os.path.join(ROOT, "build", "obj_tl" if TIMELINE else "obj")
+LIB = os.path.join(PKG, "lib", "libmacattn_tl.so" if TIMELINE else "libmacattn.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--use_fast_math", "-Xcompiler", "-fPIC,-O3",
-              "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+              "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC] + (["-DMAC_TIMELINE"] if TIMELINE else [])
 
 
 def nvcc() -> str:

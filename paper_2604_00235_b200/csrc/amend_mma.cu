@@ -17,20 +17,12 @@ bool amend_mma_supported(const MacDecodeParams& p) {
          p.page_size % 16 == 0;
 }
 
-// last warp out resets the queue counters for the next step
-__device__ __forceinline__ void amend_retire(unsigned int* ctr) {
-  __threadfence();
-  const unsigned prev = atomicAdd(ctr + 2, 1u);
-  if (prev == gridDim.x - 1) {
-    ctr[1] = 0u;
-    ctr[2] = 0u;
-  }
-}
-
 template <int ST, int MINB>  // cp.async stages per warp, min resident warps per SM (register budget)
 __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) {
   // programmatic dependent launch: wait for the front kernel's plan before touching it
+  TL_MARK(p, TL_AMEND_IN);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL_MARK(p, TL_AMEND_WAITED);
   // and let the complete kernel's grid launch as amend warps retire
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   extern __shared__ __align__(128) unsigned char smem[];
@@ -60,7 +52,8 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
     next = __reduce_max_sync(0xffffffffu, nx);
     amend_mma_item<ST>(p, it, sm, [&]() { if (next < n_items) next_it = __ldcg(list + next); });
   }
-  if (lane == 0) amend_retire(ctr);
+  TL_MARK(p, TL_AMEND_OUT);
+  // the work counters are returned to zero by the complete kernel (after this grid)
 }
 
 // Variants (stages, min warps per SM); MAC_AMEND_VARIANT selects one (development knob).

@@ -123,6 +123,11 @@ const char* mac_error_string(int code) {
 
 size_t mac_workspace_bytes(const MacDecodeParams* p) { return p ? workspace_layout(*p).total : 0; }
 
+#ifdef MAC_TIMELINE
+// development builds only (not in macattn.h): byte offset of the timeline stamps in the workspace
+size_t mac_timeline_offset(const MacDecodeParams* p) { return p ? workspace_layout(*p).tl_off : 0; }
+#endif
+
 int mac_amend_variant(const MacDecodeParams* p) {
   return (p && p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) ? 1 : 0;
 }

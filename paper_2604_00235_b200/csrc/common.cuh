@@ -181,12 +181,21 @@ __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table
 // list length and work counters) must start zeroed: the engine clears the
 // workspace once at allocation and the kernels return every counter to zero
 // by the end of each step.
+constexpr int kTlSlots = 16;
+constexpr int kMaxWsum = 128;  // scan-warp summaries per head: ceil(W / rows per CTA) * 8 warps, W <= 1024
+
+enum : int {  // timeline slots
+  TL_SCAN_IN = 0, TL_SCAN_OUT = 1, TL_VERIFY_IN = 2, TL_VERIFY_WAITED = 3, TL_VERIFY_OUT = 4,
+  TL_AMEND_IN = 5, TL_AMEND_WAITED = 6, TL_AMEND_OUT = 7, TL_COMPLETE_IN = 8, TL_COMPLETE_WAITED = 9,
+  TL_COMPLETE_OUT = 10, TL_V_SELECTED = 11, TL_V_BOUND = 12, TL_V_SURVIVED = 13, TL_V_DECIDED = 14,
+  TL_V_M = 15
+};
 struct Workspace {
   size_t mkey_off;   // [B*Hq] u64   complemented packed (dist, pos) match key
   size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
   size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
-  size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter, 2 amend done counter,
-                     //              (3-15 spare)
+  size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter (both reset by complete),
+                     //              (2-15 spare)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  splits planned for the group
   size_t mpos_off;   // [B] i32      position m of this step
@@ -196,6 +205,9 @@ struct Workspace {
   size_t qrot_off;   // [B*Hq*d]     rotated queries (math dtype)
   size_t part_off;   // [B*Hq*max_chunks*2*(d_v+1)] split partial summaries
   size_t hpart_off;  // [B*Hq*W] f32  two-pass match: distance over the first d/2 dims per ring row
+  size_t wsum_off;   // [B*Hq*kMaxWsum] uint4  two-pass match: per scan warp {P1, slot1, P2, slot2},
+                     //                 its two smallest partials (fp32 bits) and their ring slots
+  size_t tl_off;     // [kTlSlots][2] u64 timeline stamps (MAC_TIMELINE builds only)
   size_t total;
 };
 __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -216,13 +228,38 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.qrot_off = align256(w.list_off + 16 * groups * p.max_chunks);
   w.part_off = align256(w.qrot_off + acc * rows * p.head_dim);
   w.hpart_off = align256(w.part_off + acc * rows * p.max_chunks * 2 * (p.head_dim_v + 1));
-  w.total = align256(w.hpart_off + 4 * rows * (size_t)p.window);
+  w.wsum_off = align256(w.hpart_off + 4 * rows * (size_t)p.window);
+  w.tl_off = align256(w.wsum_off + 16 * rows * (size_t)kMaxWsum);
+#ifdef MAC_TIMELINE
+  w.total = align256(w.tl_off + 16 * kTlSlots);
+#else
+  w.total = w.tl_off;
+#endif
   return w;
 }
 
 template <typename T> __host__ __device__ __forceinline__ T* ws_ptr(const MacDecodeParams& p, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(p.workspace) + off);
 }
+
+// development timeline (MAC_TIMELINE builds): per slot, the earliest and latest
+// %globaltimer stamp over the CTAs that reach the mark (thread 0 of each CTA)
+#ifdef MAC_TIMELINE
+__device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  unsigned long long* tl = ws_ptr<unsigned long long>(p, workspace_layout(p).tl_off) + 2 * slot;
+  atomicMin(tl, t);
+  atomicMax(tl + 1, t);
+}
+#define TL_MARK(p, slot) tl_mark((p), (slot))
+// stamp once `v` (a loaded value) is available
+#define TL_MARK_DEP(p, slot, v) do { asm volatile("" :: "r"(v)); tl_mark((p), (slot)); } while (0)
+#else
+#define TL_MARK(p, slot) ((void)0)
+#define TL_MARK_DEP(p, slot, v) ((void)0)
+#endif
 
 // Plan one GQA group: split grid over [grid_start(lo_g), m] and one work item
 // {grp, c, t0, t1} per split appended to the device work list (the paper's

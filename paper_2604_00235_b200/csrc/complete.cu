@@ -8,12 +8,19 @@ namespace mac {
 template <int MODE>
 __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, int full_mode) {
   // programmatic dependent launch: the grid is set up while the amend kernel drains
+  TL_MARK(p, TL_COMPLETE_IN);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL_MARK(p, TL_COMPLETE_WAITED);
   const int bh = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (bh < p.batch * p.n_q_heads) complete_head<MODE>(p, bh, full_mode);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // work list consumed
+#ifdef MAC_TIMELINE
+  __syncthreads();
+#endif
+  TL_MARK(p, TL_COMPLETE_OUT);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // work list consumed: list length and amend claim counter
     unsigned int* ctr = ws_ptr<unsigned int>(p, workspace_layout(p).ctr_off);
     ctr[0] = 0u;
+    ctr[1] = 0u;
   }
 }
 

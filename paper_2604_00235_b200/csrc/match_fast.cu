@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  TL_MARK(p, TL_SCAN_IN);
   if ((int)blockIdx.x < n_append) {
     const int i = blockIdx.x * (kThreads / 32) + warp;
     if (i < p.batch * p.n_kv_heads) append_warp(p, i, rotate_only, plan);
@@ -221,120 +222,133 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   const int slot = row0 + k * 32 + warp * 4 + quad;
   const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
   const bool live = slot < W && last >= 1 && pos >= first;
-  if ((sub & ((1 << kShift) - 1)) == 0 && slot < W) hpart[slot] = live ? part[0] : CUDART_INF_F;
+  const bool holder = (sub & ((1 << kShift) - 1)) == 0 && slot < W;
+  const float pv = live ? part[0] : CUDART_INF_F;
+  if (holder) hpart[slot] = pv;
+  // this warp's summary for pass 2: its two smallest partials (non-negative fp32, so they
+  // order as unsigned bits; dead rows and duplicate lanes are +inf) and their slots
+  const unsigned bits = holder ? __float_as_uint(pv) : 0x7f800000u;
+  const unsigned w1 = __reduce_min_sync(0xffffffffu, bits);
+  const int l1 = __ffs(__ballot_sync(0xffffffffu, bits == w1)) - 1;
+  const unsigned w2 = __reduce_min_sync(0xffffffffu, lane == l1 ? 0xffffffffu : bits);
+  const int l2 = __ffs(__ballot_sync(0xffffffffu, bits == w2 && lane != l1)) - 1;
+  const int s1 = __shfl_sync(0xffffffffu, slot, l1), s2 = __shfl_sync(0xffffffffu, slot, l2 < 0 ? l1 : l2);
+  if (lane == 0) {
+    uint4* wsum = ws_ptr<uint4>(p, workspace_layout(p).wsum_off) + (int64_t)bh * kMaxWsum;
+    wsum[split * (kThreads / 32) + warp] = make_uint4(w1, (unsigned)s1, l2 < 0 ? 0x7f800000u : w2, (unsigned)s2);
+  }
+  TL_MARK(p, TL_SCAN_OUT);
 }
 
-// Pass 2: one CTA per GQA group (request, kv head), 8 warps: 8/g warps per head,
-// each owning a contiguous share of the head's ring rows.
-//   1. every warp takes the two smallest partials of its share as candidates and
-//      completes their distances (their second halves, one load round);
-//   2. the head's bound D* = the smallest candidate distance (shared memory);
-//   3. every warp completes the distances of the other rows of its share with
-//      P(r) <= D* (usually none on the hit path);
-//   4. per head: exact argmin over candidates and survivors, decide_one; the
-//      group is planned in the same CTA (no cross-CTA arrival).
-// PER_HEAD: one CTA per (request, head) instead (8 warps on one head's rows) when there are
-// fewer GQA groups than SMs but enough heads; the group is then planned by its last-decided
-// head (decide_head's arrival count).
+// Pass 2: one warp per head (a CTA per GQA group, or a CTA per head with PER_HEAD).
+//   1. one load round: the head's scan-warp summaries (each scan warp's two smallest
+//      partials and their slots), the second-half query dims, seq_lens;
+//   2. candidates = the head's two smallest partials; their full distances (the second
+//      halves of two ring rows) give the bound D* >= min D;
+//   3. a scan warp's rows can hold a survivor (P <= D*, not a candidate) only if its
+//      second-smallest partial is <= D*, or its smallest is and is not a candidate; only
+//      those warps' partials are read and their survivors completed (usually none on the
+//      hit path, all of them for a fresh query);
+//   4. exact argmin (ties -> larger position, matching.py:171-173), decide; the group is
+//      planned by its CTA (or by its last-decided head with PER_HEAD).
+// rows: ring rows per scan CTA of the launched scan variant (its warps cover rows*4/32 rows each).
 template <bool PER_HEAD>
-__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows) {
+  TL_MARK(p, TL_VERIFY_IN);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL_MARK(p, TL_VERIFY_WAITED);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
   const int grp = PER_HEAD ? blockIdx.x / g : blockIdx.x;
-  const int wph = PER_HEAD ? 8 : 8 / g;           // warps per head
-  const int hl = PER_HEAD ? blockIdx.x % g : warp / wph, part = PER_HEAD ? warp : warp % wph;
-  const bool active = PER_HEAD || hl < g;
+  const int hl = PER_HEAD ? blockIdx.x % g : warp;
   const int b = grp / Hkv, kvh = grp % Hkv;
-  const int bh = b * Hq + kvh * g + (active ? hl : 0);
+  const int bh = b * Hq + kvh * g + hl;
+  const int nsum = ((W + rows - 1) / rows) * (kThreads / 32);  // scan warps of this head
+  const int loads = rows / 32;                                 // row groups per scan warp
+  const float* hpart = ws_ptr<const float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
+  const uint4* wsum = ws_ptr<const uint4>(p, workspace_layout(p).wsum_off) + (int64_t)bh * kMaxWsum;
+  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
+  const int sub = lane & 7, quad = lane >> 3;
+  constexpr int kSumPerLane = kMaxWsum / 32;
+  uint4 sm[kSumPerLane];
+#pragma unroll
+  for (int i = 0; i < kSumPerLane; ++i) {
+    const int j = lane + 32 * i;
+    sm[i] = j < nsum ? __ldcg(wsum + j) : make_uint4(0x7f800000u, 0u, 0x7f800000u, 0u);
+  }
+  float qh[8];  // second-half query dims of this lane's 8-lane row group
+#pragma unroll
+  for (int i = 0; i < 8; ++i) qh[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + 64 + sub * 8 + i, p.in_dtype);
   const int m = p.seq_lens[b] + 1;
+  TL_MARK_DEP(p, TL_V_M, m);
+  // 1. the head's two smallest partials: this lane's best two of its summaries, then the warp's
+  unsigned a1 = 0x7f800000u, a2 = 0x7f800000u, t1 = 0u, t2 = 0u;
+#pragma unroll
+  for (int i = 0; i < kSumPerLane; ++i) {
+    if (sm[i].x < a1) { a2 = a1; t2 = t1; a1 = sm[i].x; t1 = sm[i].y; }
+    else if (sm[i].x < a2) { a2 = sm[i].x; t2 = sm[i].y; }
+    if (sm[i].z < a2) { a2 = sm[i].z; t2 = sm[i].w; }
+  }
+  const unsigned w1 = __reduce_min_sync(0xffffffffu, a1);
+  const int lane1 = __ffs(__ballot_sync(0xffffffffu, a1 == w1)) - 1;
+  const unsigned mine2 = lane == lane1 ? a2 : a1;
+  const unsigned w2 = __reduce_min_sync(0xffffffffu, mine2);
+  const int lane2 = __ffs(__ballot_sync(0xffffffffu, mine2 == w2)) - 1;
+  const int cs1 = w1 < 0x7f800000u ? (int)__shfl_sync(0xffffffffu, t1, lane1) : -1;
+  const unsigned ts2 = __shfl_sync(0xffffffffu, lane == lane1 ? t2 : t1, lane2);
+  const int cs2 = w2 < 0x7f800000u ? (int)ts2 : -1;
+  // step geometry (needs m)
   int first = m - W;
   if (first < 1) first = 1;
   if (p.delta_max > 0 && m - p.delta_max > first) first = m - p.delta_max;
   const int last = m - 1;
   const int n_scan = last >= first ? last - first + 1 : 0;
   const int cur_slot = last >= 1 ? (last - 1) % W : 0;
-  const int share = (W + wph - 1) / wph;
-  const int r0 = part * share, r1 = min(W, r0 + share);
-  const float* hpart = ws_ptr<const float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
-  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
-  const int sub = lane & 7, quad = lane >> 3;
-  float qh[8];  // second-half query dims of this lane's 8-lane row group
-#pragma unroll
-  for (int i = 0; i < 8; ++i) qh[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + 64 + sub * 8 + i, p.in_dtype);
   auto pos_of = [&](int slot) { return last - cur_slot + slot - (slot > cur_slot ? W : 0); };
   auto key_of = [&](float d, int slot) {
     return ~(((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos_of(slot)));
   };
-  // every partial of this lane's share, all loads in flight at once (a share is at most
-  // W <= 1024 rows, launch_front_bf16 checks); L1-allocating loads, so the survivor pass
-  // below re-reads them from L1
-  constexpr int kPer = 32;
-  float prv[kPer];
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int slot = r0 + i * 32 + lane;
-    prv[i] = (active && slot < r1) ? hpart[slot] : CUDART_INF_F;
-  }
-  // 1. two smallest partials of this warp's share
-  float p1 = CUDART_INF_F, p2 = CUDART_INF_F;
-  int s1 = -1, s2 = -1;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const float pr = prv[i];
-    const int slot = r0 + i * 32 + lane;
-    if (pr < p1) { p2 = p1; s2 = s1; p1 = pr; s1 = slot; }
-    else if (pr < p2) { p2 = pr; s2 = slot; }
-  }
-  float c1 = p1;
-  int cs1 = s1;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, c1, o);
-    const int os = __shfl_xor_sync(0xffffffffu, cs1, o);
-    if (ob < c1 || (ob == c1 && os > cs1)) { c1 = ob; cs1 = os; }
-  }
-  float c2 = (s1 == cs1) ? p2 : p1;  // the lane that gave the minimum offers its runner-up
-  int cs2 = (s1 == cs1) ? s2 : s1;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, c2, o);
-    const int os = __shfl_xor_sync(0xffffffffu, cs2, o);
-    if (ob < c2 || (ob == c2 && os > cs2)) { c2 = ob; cs2 = os; }
-  }
-  // their full distances: lanes 0-7 candidate 1, lanes 8-15 candidate 2
+  TL_MARK(p, TL_V_SELECTED);
+  // 2. candidates' full distances: lanes 0-7 candidate 1, lanes 8-15 candidate 2
   const int cslot = quad == 0 ? cs1 : (quad == 1 ? cs2 : -1);
-  const float cpart = quad == 0 ? c1 : c2;
+  const float cpart = __uint_as_float(quad == 0 ? w1 : w2);
   float d2 = 0.f;
-  if (cslot >= 0 && cpart != CUDART_INF_F) d2 = dist8(qh, ld_stream(ring + (int64_t)cslot * 16 + 8 + sub));
+  if (cslot >= 0) d2 = dist8(qh, ld_stream(ring + (int64_t)cslot * 16 + 8 + sub));
   d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
   d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
   d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
-  const bool cvalid = cslot >= 0 && cpart != CUDART_INF_F;
-  const float cfull = cvalid ? cpart + d2 : CUDART_INF_F;
-  unsigned long long key = (cvalid && sub == 0 && quad < 2) ? key_of(cfull, cslot) : 0ull;
-  float dmin = fminf(__shfl_sync(0xffffffffu, cfull, 0), __shfl_sync(0xffffffffu, cfull, 8));
-  // 2. the head's bound
-  __shared__ float sD[8];
-  __shared__ unsigned long long skey[8];
-  __shared__ int slo[8];
-  if (lane == 0) sD[warp] = dmin;
-  __syncthreads();
-  float D = CUDART_INF_F;
-  const int w0 = PER_HEAD ? 0 : hl * wph;
-  for (int w = w0; w < w0 + wph && w < 8; ++w) D = fminf(D, sD[w]);
-  // 3. other rows of the share that can still beat D*: 8 lanes per row, up to 8 rows per
-  //    lane group in flight (32 per warp per round; a fresh query makes every row survive)
-  if (active && D != CUDART_INF_F) {
+  const float cfull = cslot >= 0 ? cpart + d2 : CUDART_INF_F;
+  unsigned long long key = (cslot >= 0 && sub == 0 && quad < 2) ? key_of(cfull, cslot) : 0ull;
+  const float D = fminf(__shfl_sync(0xffffffffu, cfull, 0), __shfl_sync(0xffffffffu, cfull, 8));
+  TL_MARK(p, TL_V_BOUND);
+  // 3. scan warps that can hold a survivor (exact test per row inside)
+  const unsigned Dbits = __float_as_uint(D);
+  unsigned need = 0u;  // bit i: summary lane + 32 i
+  if (D != CUDART_INF_F) {
+#pragma unroll
+    for (int i = 0; i < kSumPerLane; ++i) {
+      const bool c1 = (int)sm[i].y == cs1 || (int)sm[i].y == cs2;
+      const bool n = sm[i].z <= Dbits || (sm[i].x <= Dbits && !c1);
+      need |= n ? (1u << i) : 0u;
+    }
+  }
 #pragma unroll 1
-    for (int base = r0; base < r1; base += 32) {
-      const int slot = base + lane;
-      const float pr = slot < r1 ? hpart[slot] : CUDART_INF_F;
-      const bool surv = pr <= D && pr != CUDART_INF_F && slot != cs1 && slot != cs2;
-      unsigned mask = __ballot_sync(0xffffffffu, surv);
-      if (!mask) continue;
-      // lane group `quad` takes survivors quad, quad+4, quad+8, ... of this chunk
+  for (int i = 0; i < kSumPerLane; ++i) {
+    unsigned warps_i = __ballot_sync(0xffffffffu, (need >> i) & 1u);
+#pragma unroll 1
+    while (warps_i) {
+      const int j = 32 * i + __ffs(warps_i) - 1;  // scan warp j = split * 8 + w
+      warps_i &= warps_i - 1;
+      // its rows: split * rows + k * 32 + w * 4 + q, k < loads, q < 4 (lane = k * 4 + q)
+      const int jsplit = j / (kThreads / 32), jw = j % (kThreads / 32);
+      auto slot_of = [&](int l) { return jsplit * rows + (l >> 2) * 32 + jw * 4 + (l & 3); };
+      const int my = slot_of(lane);
+      const bool mine_ok = lane < loads * 4 && my < W;
+      const float pr = mine_ok ? hpart[my] : CUDART_INF_F;
+      const bool surv = pr <= D && pr != CUDART_INF_F && my != cs1 && my != cs2;
+      const unsigned mask = __ballot_sync(0xffffffffu, surv);
+      // lane group `quad` takes survivors quad, quad+4, quad+8, ... of this warp's rows
       int li[8];
       uint4 rv[8];
 #pragma unroll
@@ -344,7 +358,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
         unsigned mm = mask;
         for (; n > 0 && mm; --n) mm &= mm - 1;
         if (mm) li[k] = __ffs(mm) - 1;
-        rv[k] = li[k] >= 0 ? ld_stream(ring + (int64_t)(base + li[k]) * 16 + 8 + sub) : make_uint4(0, 0, 0, 0);
+        rv[k] = li[k] >= 0 ? ld_stream(ring + (int64_t)slot_of(li[k]) * 16 + 8 + sub) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -354,53 +368,56 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p) {
         e += __shfl_xor_sync(0xffffffffu, e, 1);
         const float prs = __shfl_sync(0xffffffffu, pr, li[k] >= 0 ? li[k] : 0);
         if (li[k] >= 0 && sub == 0) {
-          const unsigned long long k2 = key_of(prs + e, base + li[k]);
+          const unsigned long long k2 = key_of(prs + e, slot_of(li[k]));
           key = k2 > key ? k2 : key;
         }
       }
     }
   }
-  // 4. per head: exact argmin, decision; the group's plan
+  TL_MARK(p, TL_V_SURVIVED);
+  // 4. exact argmin, decision; the group's plan
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
     key = other > key ? other : key;
   }
-  if (lane == 0) skey[warp] = key;
-  __syncthreads();
-  if (active && part == 0 && lane == 0) {
-    for (int w = w0 + 1; w < w0 + wph; ++w) key = skey[w] > key ? skey[w] : key;
-    double bd = CUDART_INF;
-    int bpos = -1;
-    if (key) {
-      const unsigned long long raw = ~key;
-      bd = (double)__uint_as_float((unsigned)(raw >> 32));
-      bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
-    }
-    if (PER_HEAD) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos);  // the group's last head plans it
-    else slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
+  double bd = CUDART_INF;
+  int bpos = -1;
+  if (key) {
+    const unsigned long long raw = ~key;
+    bd = (double)__uint_as_float((unsigned)(raw >> 32));
+    bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
   }
-  if (PER_HEAD) return;
+  if (PER_HEAD) {
+    if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos);  // the group's last head plans it
+    TL_MARK(p, TL_VERIFY_OUT);
+    return;
+  }
+  __shared__ int slo[8];
+  if (lane == 0) slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
   __syncthreads();
-  if (tid == 0) {
+  TL_MARK(p, TL_V_DECIDED);
+  if (threadIdx.x == 0) {
     int lo_g = m;
     for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
     __threadfence();
     plan_group(p, b, kvh, m, lo_g);
   }
+  TL_MARK(p, TL_VERIFY_OUT);
 }
 
-cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head) {
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(per_head ? 32 : 32 * (p.n_q_heads / p.n_kv_heads));
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true>, p) : cudaLaunchKernelEx(&cfg, verify_kernel<false>, p);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true>, p, rows)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false>, p, rows);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -455,7 +472,7 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
-  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st, per_head);
+  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st, per_head, u.rows);
   return cudaSuccess;
 }
 

@@ -1,0 +1,96 @@
+"""In-step kernel timeline of the C3 decode step (development tool).
+
+Runs the C3 hit-path workload of bench.py through the MAC_TIMELINE build of the
+library (lib/libmacattn_tl.so: every kernel stamps %globaltimer at entry, after its
+grid-dependency wait, and at exit, min and max over CTAs) and prints, per kernel,
+when its first / last CTA entered, got past the wait and left, relative to the
+first scan CTA, averaged over the steps.
+
+    MAC_TIMELINE=1 python -m paper_2604_00235_b200.build
+    python tools/timeline.py [--steps 10] [--batch 32] [--ctx 131072]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ["MACATTN_LIB"] = os.path.join(ROOT, "paper_2604_00235_b200", "lib", "libmacattn_tl.so")
+sys.path.insert(0, ROOT)
+
+SLOTS = ["scan_in", "scan_out", "verify_in", "verify_waited", "verify_out", "amend_in", "amend_waited",
+         "amend_out", "complete_in", "complete_waited", "complete_out", "v_selected", "v_bound", "v_survived", "v_decided", "v_m"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--max-chunks", type=int, default=0)
+    ap.add_argument("--min-chunk", type=int, default=128)
+    a = ap.parse_args()
+    import bench
+
+    S = a.steps + 2
+    n0 = a.ctx - S - 1
+    states = bench.make_states(list(range(a.batch)), n0=n0, steps=S, hq=32, hkv=8, d=bench.D, dv=bench.D,
+                               window=bench.WINDOW, band=bench.BAND)
+    import torch
+
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, _lib
+    from paper_2604_00235_b200.synth import inject_into_engine
+
+    dev = torch.device("cuda", 0)
+    cfg = EngineConfig(d=bench.D, d_v=bench.D, n_q_heads=32, n_kv_heads=8, window=bench.WINDOW, band=bench.BAND,
+                       tau=bench.TAU, storage="bf16")
+    eng = BatchDecodeEngine(cfg, a.batch, a.ctx + 64, device=dev, max_chunks=a.max_chunks or None,
+                            min_chunk=a.min_chunk)
+    inject_into_engine(eng, 0, states, n0, bulk_seed=0)
+    lib = _lib.load()
+    lib.mac_timeline_offset.restype = ctypes.c_size_t
+    lib.mac_timeline_offset.argtypes = [ctypes.POINTER(_lib.MacDecodeParams)]
+    bf = torch.bfloat16
+    q_all = torch.from_numpy(np.stack([s.step_q for s in states], 1)).to(dev, bf)
+    k_all = torch.from_numpy(np.stack([s.step_k for s in states], 1)).to(dev, bf)
+    v_all = torch.from_numpy(np.stack([s.step_v for s in states], 1)).to(dev, bf)
+    P = eng._params(0, q_all[0], k_all[0], v_all[0], _lib.DT_BF16)
+    off = int(lib.mac_timeline_offset(P))
+    tl = eng.workspace[off:off + 16 * 16].view(torch.int64).view(16, 2)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    rows = []
+    for s in range(S):
+        tl[:, 0] = torch.iinfo(torch.int64).max
+        tl[:, 1] = 0
+        if not a.no_flush:
+            flush.zero_()
+        torch.cuda._sleep(200_000)
+        eng.decode_step(0, q_all[s], k_all[s], v_all[s])
+        torch.cuda.synchronize()
+        t = tl.cpu().numpy().astype(np.float64)
+        if s >= 2:
+            rows.append(t)
+    t = np.stack(rows)  # [steps, 16, 2] ns
+    base = t[:, 0, 0][:, None, None]
+    rel = (t - base) / 1e3  # us
+    out = {}
+    for i, name in enumerate(SLOTS):
+        first, last = rel[:, i, 0], rel[:, i, 1]
+        ok = t[:, i, 1] > 0
+        if ok.any():
+            out[name] = (round(float(first[ok].mean()), 2), round(float(last[ok].mean()), 2))
+    print(json.dumps({"batch": a.batch, "ctx": a.ctx, "max_chunks": eng.max_chunks, "min_chunk": a.min_chunk, "hit_rate": float(eng.o_use.float().mean()),
+                      "first_last_us": out}))
+    for name, (f, l) in out.items():
+        print(f"{name:16s} first {f:8.2f}  last {l:8.2f}")
+
+
+if __name__ == "__main__":
+    main()
