@@ -525,6 +525,7 @@ def run_c4(args, wl):
     e.ring_q[0][0][:, slots_r] = torch.from_numpy(st.ring_q).to(dev, e.sdt)
     e.ring_acc[0][0][:, slots_r] = torch.from_numpy(st.ring_acc).to(dev, e.sumdt)
     e.ring_lse[0][0][:, slots_r] = torch.from_numpy(st.ring_lse).to(dev, e.sumdt)
+    e.sync_ring_q32(0)
     e.seq_lens[0].fill_(n0)
     bf = torch.bfloat16
     q_all = torch.from_numpy(st.step_q[:, None]).to(dev, bf)

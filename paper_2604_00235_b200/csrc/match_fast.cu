@@ -156,11 +156,17 @@ __device__ __forceinline__ float dist8_f2(const unsigned long long* q2, uint4 c)
 // ring bytes; when nearly every row survives (a fresh query, all distances
 // ~2d) pass 2 reads the second halves of all rows — the one-pass bytes.  The
 // distance is the one-pass kernel's fp32 sum of squares split in two sums.
-template <int kRowsPerCta, int kMinBlocks>
+// PLANAR (kQDims = 32): the rows are read from ring_q32, 64 contiguous bytes per row
+// (a contiguous 64 KiB stream per head) instead of the strided 64-byte prefixes of ring_q.
+template <int kRowsPerCta, int kMinBlocks, int kQDims, bool PLANAR = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDecodeParams p, int n_match,
                                                                           int do_append, int rotate_only, int plan,
                                                                           int /*unused*/) {
-  constexpr int kLoads = kRowsPerCta / 32;  // 8 lanes per row, 4 rows per warp-load
+  constexpr int LPR = kQDims / 8;                    // lanes per row (16 B = 8 dims each)
+  constexpr int RPW = 32 / LPR;                      // rows per warp-load
+  constexpr int kLoads = kRowsPerCta / (8 * RPW);    // loads per lane
+  static_assert(kLoads >= LPR && kLoads % LPR == 0 && (LPR == 8 || LPR == 4), "reduce-scatter layout");
+  constexpr int NF = kLoads / LPR;                   // rows each lane ends up holding
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -175,16 +181,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   const int bh = (blockIdx.x - n_append) / nsplit, split = (blockIdx.x - n_append) % nsplit;
   const int b = bh / p.n_q_heads;
   const int m = p.seq_lens[b] + 1;
-  const int sub = lane & 7, quad = lane >> 3;
-  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
+  const int sub = lane % LPR, quad = lane / LPR;
+  static_assert(!PLANAR || kQDims == 32, "ring_q32 holds 32 dims");
+  constexpr int kRowU4 = PLANAR ? 4 : 16;  // uint4 per row of the source
+  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(PLANAR ? p.ring_q32 : p.ring_q) +
+                                                     (int64_t)bh * W * (kRowU4 * 8));
   const int row0 = split * kRowsPerCta;
   uint4 v[kLoads];
 #pragma unroll
   for (int k = 0; k < kLoads; ++k) {
-    const int slot = row0 + k * 32 + warp * 4 + quad;
-    v[k] = slot < W ? ld_stream(ring + (int64_t)slot * 16 + sub) : make_uint4(0, 0, 0, 0);
+    const int slot = row0 + k * 8 * RPW + warp * RPW + quad;
+    v[k] = slot < W ? ld_stream(ring + (int64_t)slot * kRowU4 + sub) : make_uint4(0, 0, 0, 0);
   }
-  unsigned long long q2[4];  // this lane's 8 first-half query dims, as fp32 pairs
+  unsigned long long q2[4];  // this lane's 8 query dims, as fp32 pairs
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     q2[i] = f2_pack((float)load_in(p.q_pre, (int64_t)bh * 128 + sub * 8 + 2 * i, p.in_dtype),
@@ -198,62 +207,68 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   float part[kLoads];
 #pragma unroll
   for (int k = 0; k < kLoads; ++k) part[k] = dist8_f2(q2, v[k]);
-  // reduce-scatter over the row's 8 lanes (kLoads = 8: one shuffle per row instead of
-  // three): after the xor-4, -2, -1 rounds lane `sub` holds the full partial of row k = sub
-  static_assert(kLoads == 8 || kLoads == 4 || kLoads == 2, "reduce-scatter layout");
+  // reduce-scatter over the row's LPR lanes: each xor round halves the values a lane keeps;
+  // afterwards lane `sub` holds the partials of rows kbase + i, i < NF
+  int kbase = 0;
 #pragma unroll
-  for (int o = 4, n = kLoads; o > 0; o >>= 1) {
-    if (n > 1) {
-      const bool up = sub & o;
+  for (int o = LPR / 2, n = kLoads; o > 0; o >>= 1) {
+    const bool up = sub & o;
 #pragma unroll
-      for (int i = 0; i < n / 2; ++i) {
-        const float send = up ? part[i] : part[i + n / 2];
-        const float keep = up ? part[i + n / 2] : part[i];
-        part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-      n >>= 1;
-    } else {
-      part[0] += __shfl_xor_sync(0xffffffffu, part[0], o);
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = up ? part[i] : part[i + n / 2];
+      const float keep = up ? part[i + n / 2] : part[i];
+      part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
+    kbase += up ? n / 2 : 0;
+    n >>= 1;
   }
-  // lane `sub` now holds row k = sub >> (3 - log2(kLoads)) (kLoads < 8: lanes pair up)
-  constexpr int kShift = kLoads == 8 ? 0 : (kLoads == 4 ? 1 : 2);
-  const int k = sub >> kShift;
-  const int slot = row0 + k * 32 + warp * 4 + quad;
-  const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
-  const bool live = slot < W && last >= 1 && pos >= first;
-  const bool holder = (sub & ((1 << kShift) - 1)) == 0 && slot < W;
-  const float pv = live ? part[0] : CUDART_INF_F;
-  if (holder) hpart[slot] = pv;
-  // this warp's summary for pass 2: its two smallest partials (non-negative fp32, so they
-  // order as unsigned bits; dead rows and duplicate lanes are +inf) and their slots
-  const unsigned bits = holder ? __float_as_uint(pv) : 0x7f800000u;
-  const unsigned w1 = __reduce_min_sync(0xffffffffu, bits);
-  const int l1 = __ffs(__ballot_sync(0xffffffffu, bits == w1)) - 1;
-  const unsigned w2 = __reduce_min_sync(0xffffffffu, lane == l1 ? 0xffffffffu : bits);
-  const int l2 = __ffs(__ballot_sync(0xffffffffu, bits == w2 && lane != l1)) - 1;
-  const int s1 = __shfl_sync(0xffffffffu, slot, l1), s2 = __shfl_sync(0xffffffffu, slot, l2 < 0 ? l1 : l2);
+  // hpart and this warp's summary for pass 2: its two smallest partials (non-negative fp32,
+  // so they order as unsigned bits; dead rows are +inf) and their slots
+  unsigned a1 = 0x7f800000u, a2 = 0x7f800000u;
+  int t1 = 0, t2 = 0;
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    const int slot = row0 + (kbase + i) * 8 * RPW + warp * RPW + quad;
+    const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
+    const bool live = slot < W && last >= 1 && pos >= first;
+    const float pv = live ? part[i] : CUDART_INF_F;
+    if (slot < W) hpart[slot] = pv;
+    const unsigned bits = __float_as_uint(pv);
+    if (bits < a1) { a2 = a1; t2 = t1; a1 = bits; t1 = slot; }
+    else if (bits < a2) { a2 = bits; t2 = slot; }
+  }
+  const unsigned w1 = __reduce_min_sync(0xffffffffu, a1);
+  const int l1 = __ffs(__ballot_sync(0xffffffffu, a1 == w1)) - 1;
+  const unsigned mine2 = lane == l1 ? a2 : a1;
+  const unsigned w2 = __reduce_min_sync(0xffffffffu, mine2);
+  const int l2 = __ffs(__ballot_sync(0xffffffffu, mine2 == w2)) - 1;
+  const int s1 = __shfl_sync(0xffffffffu, t1, l1);
+  const int s2 = __shfl_sync(0xffffffffu, lane == l1 ? t2 : t1, l2);
   if (lane == 0) {
     uint4* wsum = ws_ptr<uint4>(p, workspace_layout(p).wsum_off) + (int64_t)bh * kMaxWsum;
-    wsum[split * (kThreads / 32) + warp] = make_uint4(w1, (unsigned)s1, l2 < 0 ? 0x7f800000u : w2, (unsigned)s2);
+    wsum[split * (kThreads / 32) + warp] = make_uint4(w1, (unsigned)s1, w2, (unsigned)s2);
   }
   TL_MARK(p, TL_SCAN_OUT);
 }
 
 // Pass 2: one warp per head (a CTA per GQA group, or a CTA per head with PER_HEAD).
 //   1. one load round: the head's scan-warp summaries (each scan warp's two smallest
-//      partials and their slots), the second-half query dims, seq_lens;
-//   2. candidates = the head's two smallest partials; their full distances (the second
-//      halves of two ring rows) give the bound D* >= min D;
+//      partials and their slots), the remaining query dims, seq_lens;
+//   2. candidates = the head's two smallest partials; their full distances (the remaining
+//      dims of two ring rows) give the bound D* >= min D;
 //   3. a scan warp's rows can hold a survivor (P <= D*, not a candidate) only if its
 //      second-smallest partial is <= D*, or its smallest is and is not a candidate; only
 //      those warps' partials are read and their survivors completed (usually none on the
 //      hit path, all of them for a fresh query);
 //   4. exact argmin (ties -> larger position, matching.py:171-173), decide; the group is
 //      planned by its CTA (or by its last-decided head with PER_HEAD).
-// rows: ring rows per scan CTA of the launched scan variant (its warps cover rows*4/32 rows each).
-template <bool PER_HEAD>
+// rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
+template <bool PER_HEAD, int kQDims>
 __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows) {
+  constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
+  constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
+  constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
+  constexpr int G = 32 / LR;                       // rows per warp-round
   TL_MARK(p, TL_VERIFY_IN);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL_MARK(p, TL_VERIFY_WAITED);
@@ -265,11 +280,12 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   const int b = grp / Hkv, kvh = grp % Hkv;
   const int bh = b * Hq + kvh * g + hl;
   const int nsum = ((W + rows - 1) / rows) * (kThreads / 32);  // scan warps of this head
-  const int loads = rows / 32;                                 // row groups per scan warp
+  const int wrows = rows / 8;                                  // rows per scan warp
   const float* hpart = ws_ptr<const float>(p, workspace_layout(p).hpart_off) + (int64_t)bh * W;
   const uint4* wsum = ws_ptr<const uint4>(p, workspace_layout(p).wsum_off) + (int64_t)bh * kMaxWsum;
   const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
-  const int sub = lane & 7, quad = lane >> 3;
+  const int ci = lane % LR, gi = lane / LR;  // chunk of the row, row group
+  const bool cload = ci < NR;
   constexpr int kSumPerLane = kMaxWsum / 32;
   uint4 sm[kSumPerLane];
 #pragma unroll
@@ -277,11 +293,18 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     const int j = lane + 32 * i;
     sm[i] = j < nsum ? __ldcg(wsum + j) : make_uint4(0x7f800000u, 0u, 0x7f800000u, 0u);
   }
-  float qh[8];  // second-half query dims of this lane's 8-lane row group
+  float qh[8];  // the query dims of this lane's chunk (kQDims + 8 ci ..)
 #pragma unroll
-  for (int i = 0; i < 8; ++i) qh[i] = (float)load_in(p.q_pre, (int64_t)bh * 128 + 64 + sub * 8 + i, p.in_dtype);
+  for (int i = 0; i < 8; ++i)
+    qh[i] = cload ? (float)load_in(p.q_pre, (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
   const int m = p.seq_lens[b] + 1;
   TL_MARK_DEP(p, TL_V_M, m);
+  auto rest = [&](int slot) -> float {  // sum over the remaining dims of row `slot`, this row group
+    float e = (slot >= 0 && cload) ? dist8(qh, ld_stream(ring + (int64_t)slot * 16 + SPR + ci)) : 0.f;
+#pragma unroll
+    for (int o = LR / 2; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    return e;
+  };
   // 1. the head's two smallest partials: this lane's best two of its summaries, then the warp's
   unsigned a1 = 0x7f800000u, a2 = 0x7f800000u, t1 = 0u, t2 = 0u;
 #pragma unroll
@@ -310,17 +333,13 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     return ~(((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos_of(slot)));
   };
   TL_MARK(p, TL_V_SELECTED);
-  // 2. candidates' full distances: lanes 0-7 candidate 1, lanes 8-15 candidate 2
-  const int cslot = quad == 0 ? cs1 : (quad == 1 ? cs2 : -1);
-  const float cpart = __uint_as_float(quad == 0 ? w1 : w2);
-  float d2 = 0.f;
-  if (cslot >= 0) d2 = dist8(qh, ld_stream(ring + (int64_t)cslot * 16 + 8 + sub));
-  d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
-  d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
-  d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+  // 2. candidates' full distances: row group 0 candidate 1, row group 1 candidate 2
+  const int cslot = gi == 0 ? cs1 : (gi == 1 ? cs2 : -1);
+  const float cpart = __uint_as_float(gi == 0 ? w1 : w2);
+  const float d2 = rest(cslot);
   const float cfull = cslot >= 0 ? cpart + d2 : CUDART_INF_F;
-  unsigned long long key = (cslot >= 0 && sub == 0 && quad < 2) ? key_of(cfull, cslot) : 0ull;
-  const float D = fminf(__shfl_sync(0xffffffffu, cfull, 0), __shfl_sync(0xffffffffu, cfull, 8));
+  unsigned long long key = (cslot >= 0 && ci == 0 && gi < 2) ? key_of(cfull, cslot) : 0ull;
+  const float D = fminf(__shfl_sync(0xffffffffu, cfull, 0), __shfl_sync(0xffffffffu, cfull, LR));
   TL_MARK(p, TL_V_BOUND);
   // 3. scan warps that can hold a survivor (exact test per row inside)
   const unsigned Dbits = __float_as_uint(D);
@@ -340,36 +359,42 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     while (warps_i) {
       const int j = 32 * i + __ffs(warps_i) - 1;  // scan warp j = split * 8 + w
       warps_i &= warps_i - 1;
-      // its rows: split * rows + k * 32 + w * 4 + q, k < loads, q < 4 (lane = k * 4 + q)
+      // its rows: split * rows + k * 8 RPW + w * RPW + q (k < loads, q < RPW), row index l = k RPW + q
       const int jsplit = j / (kThreads / 32), jw = j % (kThreads / 32);
-      auto slot_of = [&](int l) { return jsplit * rows + (l >> 2) * 32 + jw * 4 + (l & 3); };
-      const int my = slot_of(lane);
-      const bool mine_ok = lane < loads * 4 && my < W;
-      const float pr = mine_ok ? hpart[my] : CUDART_INF_F;
-      const bool surv = pr <= D && pr != CUDART_INF_F && my != cs1 && my != cs2;
-      const unsigned mask = __ballot_sync(0xffffffffu, surv);
-      // lane group `quad` takes survivors quad, quad+4, quad+8, ... of this warp's rows
-      int li[8];
-      uint4 rv[8];
+      auto slot_of = [&](int l) { return jsplit * rows + (l / RPW) * 8 * RPW + jw * RPW + (l % RPW); };
+#pragma unroll 1
+      for (int l0 = 0; l0 < wrows; l0 += 32) {
+        const int my = slot_of(l0 + lane);
+        const bool mine_ok = l0 + lane < wrows && my < W;
+        const float pr = mine_ok ? hpart[my] : CUDART_INF_F;
+        const bool surv = pr <= D && pr != CUDART_INF_F && my != cs1 && my != cs2;
+        const unsigned mask = __ballot_sync(0xffffffffu, surv);
+        // row group gi takes survivors gi, gi + G, gi + 2G, ... of these 32 rows, 8 per round
+#pragma unroll 1
+        for (int r0 = 0; r0 < __popc(mask); r0 += 8 * G) {
+          int li[8];
+          uint4 rv[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        li[k] = -1;
-        int n = quad + 4 * k;  // the n-th set bit of mask
-        unsigned mm = mask;
-        for (; n > 0 && mm; --n) mm &= mm - 1;
-        if (mm) li[k] = __ffs(mm) - 1;
-        rv[k] = li[k] >= 0 ? ld_stream(ring + (int64_t)slot_of(li[k]) * 16 + 8 + sub) : make_uint4(0, 0, 0, 0);
-      }
+          for (int k = 0; k < 8; ++k) {
+            li[k] = -1;
+            int n = r0 + gi + G * k;  // the n-th set bit of mask
+            unsigned mm = mask;
+            for (; n > 0 && mm; --n) mm &= mm - 1;
+            if (mm) li[k] = __ffs(mm) - 1;
+            rv[k] = (li[k] >= 0 && cload) ? ld_stream(ring + (int64_t)slot_of(l0 + li[k]) * 16 + SPR + ci)
+                                          : make_uint4(0, 0, 0, 0);
+          }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float e = dist8(qh, rv[k]);
-        e += __shfl_xor_sync(0xffffffffu, e, 4);
-        e += __shfl_xor_sync(0xffffffffu, e, 2);
-        e += __shfl_xor_sync(0xffffffffu, e, 1);
-        const float prs = __shfl_sync(0xffffffffu, pr, li[k] >= 0 ? li[k] : 0);
-        if (li[k] >= 0 && sub == 0) {
-          const unsigned long long k2 = key_of(prs + e, slot_of(li[k]));
-          key = k2 > key ? k2 : key;
+          for (int k = 0; k < 8; ++k) {
+            float e = cload ? dist8(qh, rv[k]) : 0.f;
+#pragma unroll
+            for (int o = LR / 2; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            const float prs = __shfl_sync(0xffffffffu, pr, li[k] >= 0 ? li[k] : 0);
+            if (li[k] >= 0 && ci == 0) {
+              const unsigned long long k2 = key_of(prs + e, slot_of(l0 + li[k]));
+              key = k2 > key ? k2 : key;
+            }
+          }
         }
       }
     }
@@ -406,7 +431,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   TL_MARK(p, TL_VERIFY_OUT);
 }
 
-cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows) {
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads);
   cfg.blockDim = dim3(per_head ? 32 : 32 * (p.n_q_heads / p.n_kv_heads));
@@ -416,8 +441,11 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true>, p, rows)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false>, p, rows);
+  if (qdims == 32)
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -436,14 +464,16 @@ struct FrontVariant {
   void (*fn)(MacDecodeParams, int, int, int, int, int);
   int rows;
   bool two_pass;  // front_half_kernel + verify_kernel
+  int qdims;      // dims of the first pass (two-pass)
+  void (*fn_planar)(MacDecodeParams, int, int, int, int, int);  // reads ring_q32 when it is given
 };
 static const FrontVariant kFrontVariants[] = {
-    {front_half_kernel<256, 4>, 256, true},
-    {front_bf16_d128_kernel<128, 5>, 128, false},
-    {front_bf16_d128_kernel<64, 8>, 64, false},
-    {front_bf16_d128_kernel<256, 3>, 256, false},
-    {front_half_kernel<128, 5>, 128, true},
-    {front_half_kernel<64, 8>, 64, true},
+    {front_half_kernel<512, 4, 32>, 512, true, 32, front_half_kernel<512, 4, 32, true>},
+    {front_bf16_d128_kernel<128, 5>, 128, false, 0, nullptr},
+    {front_bf16_d128_kernel<64, 8>, 64, false, 0, nullptr},
+    {front_bf16_d128_kernel<256, 3>, 256, false, 0, nullptr},
+    {front_half_kernel<256, 4, 64>, 256, true, 64, nullptr},
+    {front_half_kernel<256, 4, 32>, 256, true, 32, front_half_kernel<256, 4, 32, true>},
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
@@ -468,11 +498,12 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;
   if (passes & 1) {
-    u.fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
+    auto fn = (do_match && u.fn_planar && p.ring_q32) ? u.fn_planar : u.fn;
+    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
-  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st, per_head, u.rows);
+  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st, per_head, u.rows, u.qdims);
   return cudaSuccess;
 }
 

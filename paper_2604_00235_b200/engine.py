@@ -163,6 +163,10 @@ class BatchDecodeEngine:
         self.ring_q = [torch.zeros(B, Hq, W, d, dtype=self.sdt, device=dev) for _ in range(L)]
         self.ring_acc = [torch.zeros(B, Hq, W, dv, dtype=self.sumdt, device=dev) for _ in range(L)]
         self.ring_lse = [torch.full((B, Hq, W), -math.inf, dtype=self.sumdt, device=dev) for _ in range(L)]
+        # bf16 d = 128: dims 0..31 of every ring row, contiguous per head, for the two-pass scan
+        # (kept in step by the ring write-back; call sync_ring_q32 after writing ring_q directly)
+        self.ring_q32 = ([torch.zeros(B, Hq, W, 32, dtype=self.sdt, device=dev) for _ in range(L)]
+                         if cfg.storage == "bf16" and cfg.d == 128 else None)
         self.seq_lens = [torch.zeros(B, dtype=torch.int32, device=dev) for _ in range(L)]
         i32 = dict(dtype=torch.int32, device=dev)
         self.o_out = torch.empty(B, Hq, dv, dtype=self.sumdt, device=dev)
@@ -270,6 +274,7 @@ class BatchDecodeEngine:
         P.ring_q = self.ring_q[layer].data_ptr()
         P.ring_acc = self.ring_acc[layer].data_ptr()
         P.ring_lse = self.ring_lse[layer].data_ptr()
+        P.ring_q32 = self.ring_q32[layer].data_ptr() if self.ring_q32 is not None else None
         P.rope_freqs = self.freqs.data_ptr()
         P.q_pre, P.k_pre, P.v_in = q.data_ptr(), k.data_ptr(), v.data_ptr()
         P.out = self.o_out.data_ptr()
@@ -488,6 +493,13 @@ class BatchDecodeEngine:
         self.ring_acc[layer][:, :, slots] = ring_acc.to(self.device, self.sumdt)
         self.ring_lse[layer][:, :, slots] = ring_lse.to(self.device, self.sumdt)
         self.seq_lens[layer].fill_(L)
+        self.sync_ring_q32(layer)
+
+    def sync_ring_q32(self, layer: int):
+        """Refresh the contiguous dims-0..31 copy of the query ring after ring_q was written
+        from outside the kernels (state injection)."""
+        if self.ring_q32 is not None:
+            self.ring_q32[layer].copy_(self.ring_q[layer][..., :32])
 
 
 class StepGraph:

@@ -289,3 +289,5 @@ def test_two_pass_match_large_batch_replay(B, hq, hkv):
                     worst = max(worst, rel_err(go[b, h], st.outputs[h]))
     assert hits > 0 and misses > 0
     assert worst <= TOL, worst
+    # the scan's contiguous dims-0..31 copy of the ring follows every write-back
+    assert torch.equal(eng.ring_q32[0], eng.ring_q[0][..., :32])
