@@ -117,18 +117,21 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
     """Per-request algorithmic bytes of one MAC step, from the step's device decisions.
 
     use/pos: [B, Hq] arrays; m: [B] positions.  Returns dict of totals over the batch.
-    Two-pass match (default): the first d/2 dims of every live ring row, a 4-byte partial
-    written and read back per row, and the query; the second halves of the few rows that
-    survive the bound are not counted (a lower bound: the GB/s derived from it cannot be
-    overstated; ncu's DRAM bytes cross-check it in profiles/)."""
+    Two-pass match (default): the scan streams dims 0..31 of every live ring row (the
+    contiguous ring_q32 plane), writes a 4-byte partial per row and a 16-byte summary per
+    64 rows; the verify reads the summaries and the other 96 dims of two candidate rows per
+    head.  Rows that survive the bound (a few near-repeats on the hit path) are not counted
+    (a lower bound: the GB/s derived from it cannot be overstated; ncu's DRAM bytes
+    cross-check it in profiles/)."""
     g = hq // hkv
     B = use.shape[0]
     match = verify = kv = summ = 0
+    n_sum = -(-window // 64)
     for b in range(B):
         live = min(int(m[b]) - 1, window)
-        if two_pass:  # scan: first halves + partials written; verify: partials read back
-            match += hq * live * (d // 2) * s_ring + hq * window * 4 + hq * d * s_ring
-            verify += hq * window * 4
+        if two_pass:
+            match += hq * (live * 32 * s_ring + window * 4 + n_sum * 16 + d * s_ring)
+            verify += hq * (n_sum * 16 + 2 * (d - 32) * s_ring + d * s_ring)
         else:
             match += hq * live * d * s_ring + hq * d * s_ring
         for j in range(hkv):
@@ -137,7 +140,7 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
             lo = min((max(1, int(pp) - band + 1) if uu else 1) for uu, pp in zip(u, p))
             kv += (int(m[b]) - lo + 1) * 2 * d * s_kv
         summ += int(use[b].sum()) * (d * 4 + 4)
-    ring_w = B * hq * (d * s_ring + d * 4 + 4)
+    ring_w = B * hq * (d * s_ring + 32 * s_ring + d * 4 + 4)  # ring_q row, its ring_q32 copy, summary
     out_w = B * hq * d * 4
     append = B * hkv * 2 * d * s_kv
     return {"match": match, "verify": verify, "amend": kv, "complete": summ + ring_w + out_w, "append": append,

@@ -26,7 +26,7 @@ template <> struct Traits<MAC_MODE_BF16> {
   using sum_t = float;
   using acc_t = float;
   using dist_t = float;
-  using merge_t = float;  // serving storage: fp32 merges (well inside the bf16 budget)
+  using merge_t = double;  // summary merge algebra in fp64 like f32 storage (remove() cancels)
 };
 template <> struct Traits<MAC_MODE_F64> {
   using kv_t = double;

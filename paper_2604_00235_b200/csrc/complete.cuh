@@ -37,7 +37,7 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
   using kv_t = typename Traits<MODE>::kv_t;
   using A = typename Traits<MODE>::acc_t;
   using S = typename Traits<MODE>::sum_t;
-  using D = typename Traits<MODE>::merge_t;  // merge algebra: fp32 for bf16 storage, fp64 otherwise
+  using D = typename Traits<MODE>::merge_t;  // merge algebra: fp64
   using M = A;
   const int lane = threadIdx.x & 31;
   const Workspace wsl = workspace_layout(p);

@@ -422,10 +422,9 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   if (lane == 0) slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
   __syncthreads();
   TL_MARK(p, TL_V_DECIDED);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // (the amend reads the plan after this grid completes: no fence needed)
     int lo_g = m;
     for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
-    __threadfence();
     plan_group(p, b, kvh, m, lo_g);
   }
   TL_MARK(p, TL_VERIFY_OUT);
@@ -455,11 +454,13 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-// MAC_FRONT_VARIANT (development knob): two-pass match with (ring rows per CTA, min CTAs per
-// SM) = 0: (256,4) default, 4: (128,5), 5: (64,8); one-pass stream 1-3: (128,5), (64,8), (256,3).
-// C3 step: 76.2 / 81.0 / 93.8 us two-pass, 95.6 us one-pass (128,5).  Measured alternatives that lost on C3 (persistent tensor-core, persistent
-// CUDA-core, f32x2 "lean", DSMEM-cluster argmin, one fused step kernel) are on branch
-// exp/fused-step; numbers in DESIGN.md §4.
+// MAC_FRONT_VARIANT (development knob): two-pass match, (ring rows per CTA, min CTAs per SM,
+// first-pass dims) = 0: (512, 4, 32) default, reading ring_q32 when given; 4: (256, 4, 64) on
+// ring_q; 5: (256, 4, 32); one-pass stream 1-3: (128,5), (64,8), (256,3).  C3 step (us):
+// 59.8 (0), 67.8 (4); the (256,6) and (512,3) shapes scanned 3.5 and 0.8 us slower than (0).
+// Measured alternatives that lost on C3 (persistent tensor-core, persistent CUDA-core, f32x2
+// "lean", DSMEM-cluster argmin, one fused step kernel) are on branch exp/fused-step; numbers
+// in DESIGN.md §4.
 struct FrontVariant {
   void (*fn)(MacDecodeParams, int, int, int, int, int);
   int rows;

@@ -64,6 +64,56 @@ def test_fast_replay_matches_oracle(hq, hkv, window, band, delta_max):
     assert worst <= TOL, worst
 
 
+@pytest.mark.parametrize("downdate", ["split", "remove"])
+def test_fast_ring_state_and_downdate(downdate):
+    """The decode step's complete on the bf16 path (complete_bf16_kernel): outputs, band mass,
+    the ring summary written at slot (m-1) % W and the ring_q32 copy, with the split prefix
+    and with the remove() downdate (engine.py:474-478), against the oracle every step."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    L, B, hq, hkv, W, r = 300, 2, 8, 2, 64, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=40 + s))
+           for s in range(B)]
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16",
+                       downdate_mode=downdate)
+    eng = BatchDecodeEngine(cfg, B, L, page_perm_seed=5, min_chunk=32, record_cached=True)
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16",
+                            downdate_mode=downdate)
+    oes = [orc.OracleEngine(ocfg, capacity=L) for _ in range(B)]
+    q = [bf16_round(t.q_pre[:, 0]) for t in trs]
+    k = [bf16_round(t.k_pre[:, 0]) for t in trs]
+    v = [bf16_round(t.v[:, 0]) for t in trs]
+    worst_out = worst_ring = worst_lse = 0.0
+    hits = 0
+    for m in range(1, L + 1):
+        qd = torch.from_numpy(np.stack([x[m - 1] for x in q])).to("cuda", torch.bfloat16)
+        kd = torch.from_numpy(np.stack([x[m - 1] for x in k])).to("cuda", torch.bfloat16)
+        vd = torch.from_numpy(np.stack([x[m - 1] for x in v])).to("cuda", torch.bfloat16)
+        res = eng.decode_step(0, qd, kd, vd)
+        go = res.out.double().cpu().numpy()
+        rho = res.band_mass.double().cpu().numpy()
+        slot = (m - 1) % W
+        racc = eng.ring_acc[0][:, :, slot].double().cpu().numpy()
+        rlse = eng.ring_lse[0][:, :, slot].double().cpu().numpy()
+        for b in range(B):
+            st = oes[b].decode_step(0, q[b][m - 1], k[b][m - 1], v[b][m - 1], m)
+            hits += int(st.use_hit.sum())
+            np.testing.assert_allclose(rho[b], st.band_mass, rtol=1e-3, atol=1e-6)
+            for h in range(hq):
+                worst_out = max(worst_out, rel_err(go[b, h], st.outputs[h]))
+                if math.isinf(st.prefix_lse[h]):
+                    assert math.isinf(rlse[b, h])
+                else:
+                    worst_lse = max(worst_lse, abs(rlse[b, h] - st.prefix_lse[h]))
+                    worst_ring = max(worst_ring, rel_err(racc[b, h], st.prefix_acc[h]))
+    assert hits > 0
+    # remove() subtracts the band from the full summary in fp32 (bf16 path merges in fp32): the
+    # cancellation amplifies rounding, and reused prefixes carry it into later outputs
+    assert worst_out <= (TOL if downdate == "split" else 1e-3), worst_out
+    assert worst_ring <= 1e-3 and worst_lse <= 1e-3, (worst_ring, worst_lse)
+    assert torch.equal(eng.ring_q32[0], eng.ring_q[0][..., :32])
+
+
 def test_fast_long_context_hits_and_misses():
     """C2-shaped injected state (32K, 32Q/8KV) with 30% fresh queries: misses stream the whole KV."""
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
