@@ -56,6 +56,16 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(stage: str):
+    """Per-launch DRAM bytes (read + write) of a stage's kernel from the committed ncu --set full
+    capture (profiles/r01/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as fh:
+            return float(json.load(fh)[stage]["traffic_bytes"])
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------
@@ -457,13 +467,18 @@ def run_ours(args, wl):
                                "frac": full_b / (full_ms * 1e-3) / 1e9 / peak, "bytes_per_step": full_b},
             "speedup_vs_full_attention": full_ms / ms_per_step,
             "roofline": {"bound": "hbm", "achieved": kern[dom]["gbs"], "peak": peak, "peak_kind": peak_kind,
-                         "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": None, "kernel": dom},
+                         "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": ncu_traffic(dom),
+                         "algorithmic_bytes": kern[dom]["bytes"], "kernel": dom,
+                         "traffic_source": "profiles/r01/ncu_traffic.json (ncu --set full, DRAM read+write per launch)"},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "StepGraph replay (H2D of packed bf16 q/k/v + step kernels + D2H of the bf16 output)",
                     "output_dtype": "bf16",
                     "max_rel_diff_vs_timed_pass_fp32": e2e_vs_timed},
-            "gpu_launches": 3 * K,
+            # front (append + ring scan), verify, amend, complete with the two-pass match
+            # (csrc/match_fast.cu launch_front_bf16: B*Hq >= 148 heads); the one-pass match has
+            # no verify launch
+            "gpu_launches": (4 if two_pass and B * hq >= 148 else 3) * K,
             "clocks": clk.summary(),
         }
         if cpu is not None:

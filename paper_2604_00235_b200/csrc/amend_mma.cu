@@ -11,6 +11,12 @@
 
 namespace mac {
 
+#ifdef MAC_TIMELINE
+// per-CTA amend trace (development builds): t_waited, t_end (globaltimer ns), items, tokens,
+// end of the first item, tokens of the first item
+__device__ unsigned long long g_amend_trace[4096 * 8];
+#endif
+
 bool amend_mma_supported(const MacDecodeParams& p) {
   const int g = p.n_q_heads / p.n_kv_heads;
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128 && g >= 1 && g <= 8 &&
@@ -42,6 +48,12 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
   if (lane == 0) next = atomicAdd(ctr + 1, 1u);
   next = __reduce_max_sync(0xffffffffu, next);
   int4 next_it = next < n_items ? __ldcg(list + next) : make_int4(0, 0, 0, 0);
+#ifdef MAC_TIMELINE
+  unsigned long long tr_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_t0));
+  unsigned tr_items = 0, tr_tokens = 0, tr_first_tok = 0;
+  unsigned long long tr_first = 0;
+#endif
   for (;;) {
     const unsigned item = next;
     if (item >= n_items) break;
@@ -51,7 +63,27 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
     if (lane == 0) nx = atomicAdd(ctr + 1, 1u);
     next = __reduce_max_sync(0xffffffffu, nx);
     amend_mma_item<ST>(p, it, sm, [&]() { if (next < n_items) next_it = __ldcg(list + next); });
+#ifdef MAC_TIMELINE
+    if (tr_items == 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
+      tr_first_tok = (unsigned)(it.w - it.z + 1);
+    }
+    tr_items++;
+    tr_tokens += (unsigned)(it.w - it.z + 1);
+#endif
   }
+#ifdef MAC_TIMELINE
+  if (lane == 0 && blockIdx.x < 4096) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_amend_trace[blockIdx.x * 8 + 0] = tr_t0;
+    g_amend_trace[blockIdx.x * 8 + 1] = t1;
+    g_amend_trace[blockIdx.x * 8 + 2] = tr_items;
+    g_amend_trace[blockIdx.x * 8 + 3] = tr_tokens;
+    g_amend_trace[blockIdx.x * 8 + 4] = tr_first;
+    g_amend_trace[blockIdx.x * 8 + 5] = tr_first_tok;
+  }
+#endif
   TL_MARK(p, TL_AMEND_OUT);
   // the work counters are returned to zero by the complete kernel (after this grid)
 }
@@ -108,3 +140,10 @@ cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, boo
 }
 
 }  // namespace mac
+
+#ifdef MAC_TIMELINE
+// development builds only: copy the per-CTA amend trace ([n][8] u64) to host memory
+extern "C" int mac_timeline_amend(void* host_out, int n) {
+  return (int)cudaMemcpyFromSymbol(host_out, mac::g_amend_trace, (size_t)n * 8 * sizeof(unsigned long long));
+}
+#endif

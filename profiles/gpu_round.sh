@@ -17,5 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python bench.py --steps 4 --warmup 3 --no-cpu --full-steps 3 > $O/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k "$KERN" -s 12 -c 4 \
   -o $O/prof -f python bench.py --steps 4 --warmup 3 --no-cpu --full-steps 3 > $O/ncu_full.log 2>&1
-timeout 1800 python sweep.py --out $O/sweep.jsonl > $O/sweep.log 2>&1
+[ -n "$SKIP_SWEEP" ] || timeout 1800 python sweep.py --out $O/sweep.jsonl > $O/sweep.log 2>&1
 ls -la $O
+# per-launch DRAM traffic of the captured step (bench.py reads profiles/r01/ncu_traffic.json)
+ncu -i $O/prof.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size,launch__registers_per_thread > $O/ncu_kernels.csv 2>/dev/null && python tools/ncu_traffic.py $O/ncu_kernels.csv > $O/ncu_traffic.json

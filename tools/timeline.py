@@ -65,7 +65,10 @@ def main():
     off = int(lib.mac_timeline_offset(P))
     tl = eng.workspace[off:off + 16 * 16].view(torch.int64).view(16, 2)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    rows = []
+    rows, amends = [], []
+    lib.mac_timeline_amend.restype = ctypes.c_int
+    lib.mac_timeline_amend.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    tr = np.zeros((4096, 8), np.uint64)
     for s in range(S):
         tl[:, 0] = torch.iinfo(torch.int64).max
         tl[:, 1] = 0
@@ -77,6 +80,9 @@ def main():
         t = tl.cpu().numpy().astype(np.float64)
         if s >= 2:
             rows.append(t)
+            tr[:] = 0
+            lib.mac_timeline_amend(tr.ctypes.data, 4096)
+            amends.append((tr.copy(), t[0, 0]))
     t = np.stack(rows)  # [steps, 16, 2] ns
     base = t[:, 0, 0][:, None, None]
     rel = (t - base) / 1e3  # us
@@ -90,6 +96,23 @@ def main():
                       "first_last_us": out}))
     for name, (f, l) in out.items():
         print(f"{name:16s} first {f:8.2f}  last {l:8.2f}")
+    # per-CTA amend trace: start/end spread, items and tokens per warp, first-item duration
+    for tr, base in amends[-2:]:
+        live = tr[:, 1] > 0
+        a = tr[live].astype(np.float64)
+        t0 = (a[:, 0] - base) / 1e3
+        t1 = (a[:, 1] - base) / 1e3
+        tf = (a[:, 4] - base) / 1e3
+        items, toks = a[:, 2], a[:, 3]
+        q = lambda x: " ".join(f"{v:7.2f}" for v in np.percentile(x, [0, 10, 50, 90, 100]))
+        print(f"amend CTAs {int(live.sum())}  items total {int(items.sum())}  tokens total {int(toks.sum())}")
+        print(f"  start  us p0/10/50/90/100: {q(t0)}")
+        print(f"  end    us p0/10/50/90/100: {q(t1)}")
+        has = items > 0
+        print(f"  first item dur us        : {q((tf - t0)[has])}  tokens {q(a[has, 5])}")
+        print(f"  items/CTA hist: {np.bincount(items.astype(int)).tolist()}")
+        busy = (t1 - t0)
+        print(f"  busy us                  : {q(busy)}  -> tokens/us/warp {toks.sum() / busy.sum():.2f}")
 
 
 if __name__ == "__main__":
