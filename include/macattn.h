@@ -224,6 +224,12 @@ int mac_step_stats(const MacDecodeParams* p, double* head_stats, double* group_s
 /* mass_bound_check for n_items hits; p supplies the cache geometry (storage, dims,
  * page_table, k_cache, v_cache, rope_freqs); d, d_v <= 256; no KV sharding. */
 int mac_mass_bound(const MacDecodeParams* p, const MacMassBoundParams* mb, void* stream);
+/* step I/O without the copy engines (StepGraph): the device alias of a pinned host
+ * buffer (cudaHostGetDevicePointer), and a stream-ordered copy kernel between device and
+ * pinned-host aliases, same dtype or f32 -> bf16 (MAC_DT_*); pointers 16-byte aligned,
+ * n_elems * element size a multiple of 16 (of 8 elements when narrowing). */
+int mac_host_alias(void* host, void** device_alias);
+int mac_io_copy(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, size_t n_elems, void* stream);
 
 #ifdef __cplusplus
 }

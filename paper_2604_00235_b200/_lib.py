@@ -41,6 +41,8 @@ EXPORTS = (
     "mac_prefill_kv",
     "mac_step_stats",
     "mac_mass_bound",
+    "mac_host_alias",
+    "mac_io_copy",
 )
 
 # per-head / per-group statistics fields of mac_step_stats (include/macattn.h)
@@ -171,6 +173,10 @@ def load() -> C.CDLL:
     lib.mac_step_stats.argtypes = [C.POINTER(MacDecodeParams), C.c_void_p, C.c_void_p, C.c_void_p]
     lib.mac_mass_bound.restype = C.c_int
     lib.mac_mass_bound.argtypes = [C.POINTER(MacDecodeParams), C.POINTER(MacMassBoundParams), C.c_void_p]
+    lib.mac_host_alias.restype = C.c_int
+    lib.mac_host_alias.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.mac_io_copy.restype = C.c_int
+    lib.mac_io_copy.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_size_t, C.c_void_p]
     lib.mac_merge_partials.restype = C.c_int
     lib.mac_merge_partials.argtypes = [C.POINTER(MacMergeParams), C.c_void_p]
     if lib.mac_abi_version() != ABI_VERSION:

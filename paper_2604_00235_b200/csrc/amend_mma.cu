@@ -24,16 +24,32 @@ bool amend_mma_supported(const MacDecodeParams& p) {
 }
 
 template <int ST, int MINB>  // cp.async stages per warp, min resident warps per SM (register budget)
-__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) {
-  // programmatic dependent launch: wait for the front kernel's plan before touching it
+__global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, int nb) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const uint32_t sm = smem_u32(smem);
   TL_MARK(p, TL_AMEND_IN);
+  if (nb > 0) {
+    // Split band (common.cuh band_items): the band items need only what the front kernel
+    // (the verify kernel's predecessor, complete before any of this grid launched) wrote —
+    // this step's KV row, rotated queries and positions — so they stream while the verify
+    // kernel still decides the heads.  Static assignment, one item per warp at C3.
+    const int G = p.batch * p.n_kv_heads;
+    const int* mpos = ws_ptr<const int>(p, workspace_layout(p).mpos_off);
+    for (int i = blockIdx.x; i < G * nb; i += gridDim.x) {
+      const int grp = i / nb, c = i - grp * nb;
+      const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)__ldcg(mpos + grp / p.n_kv_heads));
+      const BandItems bi = band_items(m, p.band, nb);
+      if (c >= bi.n) continue;
+      const int t0 = bi.t0 + c * bi.len;
+      amend_mma_item<ST, true>(p, make_int4(grp, c, t0, min(m, t0 + bi.len - 1)), sm, []() {});
+    }
+  }
+  // programmatic dependent launch: wait for the front kernel's plan before touching it
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL_MARK(p, TL_AMEND_WAITED);
   // and let the complete kernel's grid launch as amend warps retire
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x;
-  const uint32_t sm = smem_u32(smem);
   const Workspace w = workspace_layout(p);
   unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
   int4* list = ws_ptr<int4>(p, w.list_off);
@@ -62,7 +78,7 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
     unsigned nx = 0;
     if (lane == 0) nx = atomicAdd(ctr + 1, 1u);
     next = __reduce_max_sync(0xffffffffu, nx);
-    amend_mma_item<ST>(p, it, sm, [&]() { if (next < n_items) next_it = __ldcg(list + next); });
+    amend_mma_item<ST, false>(p, it, sm, [&]() { if (next < n_items) next_it = __ldcg(list + next); });
 #ifdef MAC_TIMELINE
     if (tr_items == 0) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
@@ -90,7 +106,7 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p) 
 
 // Variants (stages, min warps per SM); MAC_AMEND_VARIANT selects one (development knob).
 struct AmendVariant {
-  void (*fn)(MacDecodeParams);
+  void (*fn)(MacDecodeParams, int);
   int smem;
 };
 static const AmendVariant kAmendVariants[] = {
@@ -99,32 +115,68 @@ static const AmendVariant kAmendVariants[] = {
     {amend_mma_kernel<2, 8>, 2 * 2 * TILE_BYTES},
     {amend_mma_kernel<3, 8>, 3 * 2 * TILE_BYTES},
 };
+constexpr int kAmendN = (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0]));
 
 // full_spans: every group reads [1, m] (full-attention decode and its miss path), where
 // the 3-stage / 8-warps-per-SM variant measured best (C3: 2.41 vs 2.53 ms); the hit path's
 // short spans prefer 4 stages at 6 warps per SM (81.0 vs 84.5 us).  MAC_AMEND_VARIANT
 // overrides both.
-cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, bool full_spans) {
-  constexpr int kN = (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0]));
-  static int grid_full[kN] = {}, forced = -2;
+static int amend_variant(bool full_spans) {
+  static int forced = -2;
   if (forced == -2) {
     const char* env = getenv("MAC_AMEND_VARIANT");
     forced = env ? atoi(env) : -1;
-    if (forced >= kN) forced = -1;
+    if (forced >= kAmendN) forced = -1;
   }
-  const int vi = forced >= 0 ? forced : (full_spans ? 3 : 0);
-  const AmendVariant& v = kAmendVariants[vi];
+  return forced >= 0 ? forced : (full_spans ? 3 : 0);
+}
+
+// resident warps of a variant's persistent grid (sets the smem attribute on first use)
+static int amend_grid_full(int vi, cudaError_t* err) {
+  static int grid_full[kAmendN] = {};
   if (!grid_full[vi]) {
+    const AmendVariant& v = kAmendVariants[vi];
     cudaError_t e = cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) { if (err) *err = e; return 0; }
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, 32, v.smem);
     grid_full[vi] = sms * (per_sm < 1 ? 1 : per_sm);
   }
+  return grid_full[vi];
+}
+
+// Band items per GQA group for the split band (common.cuh band_items), 0 when the step does
+// not split it: the hit step of the fast path only — the two-pass front (whose verify kernel
+// the band overlaps, and which guarantees the append finished before this grid launches),
+// one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
+// (1..4).  MAC_BAND_SPLIT=0 turns it off, =n forces n items (development knobs).  The verify
+// kernel's plan and this launch call it with the same parameters, so they always agree.
+int band_split(const MacDecodeParams& p) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* env = getenv("MAC_BAND_SPLIT");
+    forced = env ? atoi(env) : -1;
+  }
+  if (forced == 0 || !amend_mma_supported(p) || !front_two_pass(p) || p.kv_offset != 0 || p.kv_limit != 0 ||
+      p.band <= 0)
+    return 0;
+  int nb = forced > 0 ? forced : amend_grid_full(amend_variant(false), nullptr) / (p.batch * p.n_kv_heads);
+  if (nb > 4 && forced < 0) nb = 4;
+  if (nb > p.max_chunks - 1) nb = p.max_chunks - 1;
+  return nb < 1 ? 0 : nb;
+}
+
+cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, bool full_spans) {
+  const int vi = amend_variant(full_spans);
+  const AmendVariant& v = kAmendVariants[vi];
+  cudaError_t err = cudaSuccess;
+  const int gfull = amend_grid_full(vi, &err);
+  if (err != cudaSuccess) return err;
+  const int nb = full_spans ? 0 : band_split(p);
   const long cap = (long)p.batch * p.n_kv_heads * p.max_chunks;
-  const int grid = (int)(grid_full[vi] < cap ? grid_full[vi] : cap);
+  const int grid = (int)(gfull < cap ? gfull : cap);
   // programmatic dependent launch: the grid is set up while the front kernel drains
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -136,7 +188,7 @@ cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, boo
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, v.fn, p);
+  return cudaLaunchKernelEx(&cfg, v.fn, p, nb);
 }
 
 }  // namespace mac

@@ -182,8 +182,10 @@ __device__ __forceinline__ void write_partial(const State& S, float* out, int se
 // One work item {grp, c, t0, t1} of the device plan: stream the group's K/V
 // rows [t0, t1] and write the piece and band partials of each of its g heads.
 // on_issued() runs once the first KV stages are in flight (the caller's
-// prefetch of its next work item hides under them).
-template <int ST, typename OnIssued>
+// prefetch of its next work item hides under them).  BAND: a split-band item
+// (common.cuh band_items), run before the plan exists — band partial only, no
+// per-head lower bound (every head's band is [max(1, m-r+1), m]).
+template <int ST, bool BAND, typename OnIssued>
 __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it, uint32_t sm, OnIssued on_issued) {
   const int lane = threadIdx.x & 31;
   const int Hkv = p.n_kv_heads, Hq = p.n_q_heads, g = Hq / Hkv, r = p.band, ps = p.page_size;
@@ -245,9 +247,9 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
     cp_commit();
   }
   on_issued();
-  const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)mpos[b]);
+  const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)__ldcg(mpos + b));
   const int cpos = m - r;
-  const int lo_h = row < g ? plan_lo[b * Hq + kvh * g + row] : (1 << 30);
+  const int lo_h = row < g ? (BAND ? 1 : __ldcg(plan_lo + b * Hq + kvh * g + row)) : (1 << 30);
   // Q fragments (hi rows 0..7, lo rows 8..15), 8 k-steps
   uint32_t qa[8][4];
   {
@@ -257,8 +259,8 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
       const int k0 = ks * 16 + q4 * 2;
       float2 x01 = make_float2(0.f, 0.f), x89 = make_float2(0.f, 0.f);
       if (row < g) {
-        x01 = *reinterpret_cast<const float2*>(qr + k0);
-        x89 = *reinterpret_cast<const float2*>(qr + k0 + 8);
+        x01 = __ldcg(reinterpret_cast<const float2*>(qr + k0));
+        x89 = __ldcg(reinterpret_cast<const float2*>(qr + k0 + 8));
       }
       float h0, l0, h1, l1, h8, l8, h9, l9;
       split_bf16(x01.x, h0, l0); split_bf16(x01.y, h1, l1);
@@ -273,7 +275,7 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
   State S;
   S.reset();
   bool in_band = false;
-  const int lo_piece = max(lo_h, t0), hi_piece = min(t1, cpos);
+  const int lo_piece = max(lo_h, t0), hi_piece = BAND ? t0 - 1 : min(t1, cpos);
   const int lo_band = max(lo_h, max(t0, cpos + 1));
   // 32-token steps: sub-tiles 2jp and 2jp+1 (stages (2jp) % ST and (2jp+1) % ST)
   // 32-token steps over sub-tile pairs (2jp, 2jp+1); an odd tail sub-tile gets a half step.

@@ -168,6 +168,42 @@ __host__ __device__ __forceinline__ Chunking group_chunking(const MacDecodeParam
   return chunking(shard_end(p, m) - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks, p.min_chunk);
 }
 
+// Split band (the bf16 fast path's hit step, launch_band_split in amend_mma.cu): the band
+// [max(1, m-r+1), m] never depends on the match (every head's lo_h <= m-r), so the amend
+// warps compute it as `nb` fixed items BEFORE their grid-dependency wait — while the verify
+// kernel decides the heads and the DRAM would otherwise idle — and the plan covers only the
+// piece [grid_start(lo_g), m-r].  Band items start on the 16-token grid below m-r+1 and
+// produce band partials only; their slots come first (0 .. n-1), the plan's piece slots
+// follow.  The planner records nb in the group's pn word (bits 16+) for the complete.
+struct BandItems {
+  int n;    // band items (slots 0 .. n-1)
+  int len;  // tokens per item (multiple of 16)
+  int t0;   // first token of item 0 (16-aligned, <= max(1, m-r+1))
+};
+__host__ __device__ __forceinline__ BandItems band_items(int m, int r, int nb) {
+  BandItems s = {0, 0, 1};
+  if (nb <= 0 || m < 1) return s;
+  const int b0 = m - r + 1 > 1 ? m - r + 1 : 1;
+  s.t0 = ((b0 - 1) & ~15) + 1;
+  const int span = m - s.t0 + 1;
+  int n = (span + 15) / 16;
+  if (n > nb) n = nb;
+  s.len = (((span + n - 1) / n) + 15) & ~15;
+  s.n = (span + s.len - 1) / s.len;
+  return s;
+}
+// the plan's split grid with the split band (nb > 0): the piece [grid_start(lo_g), m-r] in
+// at most max_chunks - nb slots; nb == 0: group_chunking
+__host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams& p, int m, int lo_g, int nb) {
+  if (nb <= 0) return group_chunking(p, m, lo_g);
+  return chunking(m - p.band - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks - nb, p.min_chunk);
+}
+// partial slots a group's complete merges, from its pn word (plan_group)
+__host__ __device__ __forceinline__ int group_slots(int pn_word, int m, int r) {
+  const int nb = pn_word >> 16;
+  return (pn_word & 0xffff) + (nb > 0 ? band_items(m, r, nb).n : 0);
+}
+
 // physical row of token t (1-based, local to this KV shard) in a paged cache
 __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table, int pages_per_seq,
                                           int b, int t, int page_size, int n_kv, int kvh) {
@@ -197,7 +233,7 @@ struct Workspace {
   size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter (both reset by complete),
                      //              (2-15 spare)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
-  size_t pn_off;     // [B*Hkv] i32  splits planned for the group
+  size_t pn_off;     // [B*Hkv] i32  piece splits planned for the group | band items requested << 16
   size_t mpos_off;   // [B] i32      position m of this step
   size_t lo_off;     // [B*Hq] i32   first token each head reads (plan)
   size_t list_off;   // [B*Hkv*max_chunks] int4 work items {grp + 1, c, t0, t1} (the amend
@@ -261,24 +297,27 @@ __device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot) {
 #define TL_MARK_DEP(p, slot, v) ((void)0)
 #endif
 
-// Plan one GQA group: split grid over [grid_start(lo_g), m] and one work item
-// {grp, c, t0, t1} per split appended to the device work list (the paper's
+// Plan one GQA group: split grid over [grid_start(lo_g), m] (or, with the split band,
+// over the piece [grid_start(lo_g), m-r] after the band slots) and one work item
+// {grp, slot, t0, t1} per split appended to the device work list (the paper's
 // load-balancer plan, built on the device with no host synchronisation).
-__device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g) {
+__device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g, int nb = 0) {
   const int start = grid_start(lo_g, p.kv_offset);
-  const int end = shard_end(p, m);
-  const Chunking ch = group_chunking(p, m, lo_g);
+  const int end = nb > 0 ? m - p.band : shard_end(p, m);
+  const Chunking ch = plan_chunking(p, m, lo_g, nb);
+  const int slot0 = nb > 0 ? band_items(m, p.band, nb).n : 0;
   const Workspace w = workspace_layout(p);
   unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
   int4* list = ws_ptr<int4>(p, w.list_off);
   const unsigned cap = (unsigned)(p.batch * p.n_kv_heads * p.max_chunks);
   const int grp = b * p.n_kv_heads + kvh;
-  ws_ptr<int>(p, w.pn_off)[grp] = ch.n;
+  ws_ptr<int>(p, w.pn_off)[grp] = ch.n | (nb << 16);
+  if (ch.n == 0) return;
   const unsigned base = atomicAdd(ctr, (unsigned)ch.n);
   const int n = (int)min((unsigned)ch.n, base < cap ? cap - base : 0u);  // full list: cannot happen
   for (int c = 0; c < n; ++c) {
     const int t0 = start + c * ch.len;
-    list[base + c] = make_int4(grp + 1, c, t0, min(end, t0 + ch.len - 1));
+    list[base + c] = make_int4(grp + 1, slot0 + c, t0, min(end, t0 + ch.len - 1));
   }
 }
 
@@ -307,7 +346,7 @@ __device__ __forceinline__ int decide_one(const MacDecodeParams& p, int bh, int 
 
 // decide_one, and the last head of a GQA group to be decided plans the group
 __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
-                                            double bdist, int bpos) {
+                                            double bdist, int bpos, int nb = 0) {
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv;
   decide_one(p, bh, m, n_scan, have, bdist, bpos);
   const Workspace w = workspace_layout(p);
@@ -322,8 +361,14 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
       const int l = __ldcg(lo + b * Hq + kvh * g + j);
       lo_g = l < lo_g ? l : lo_g;
     }
-    plan_group(p, b, kvh, m, lo_g);
+    plan_group(p, b, kvh, m, lo_g, nb);
   }
 }
+
+// host-side path decisions shared by the launchers (match_fast.cu, amend_mma.cu)
+bool match_fast_supported(const MacDecodeParams& p);
+bool front_two_pass(const MacDecodeParams& p);
+bool amend_mma_supported(const MacDecodeParams& p);
+int band_split(const MacDecodeParams& p);
 
 }  // namespace mac

@@ -62,9 +62,11 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
     lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, 8));
     lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, 16));
     lo_g = min(lo_g, m);
-    const Chunking ch = group_chunking(p, m, lo_g);
-    const int cpos = m - r;
     const int grp = b * Hkv + kvh;
+    // partial slots: the plan's split grid, after the split band's slots when the plan says so
+    const int pnw = __ldcg(ws_ptr<const int>(p, wsl.pn_off) + grp);
+    const int nsl = (pnw >> 16) ? group_slots(pnw, m, r) : group_chunking(p, m, lo_g).n;
+    const int cpos = m - r;
     const float* pbase = ws_ptr<const float>(p, wsl.part_off) + ((int64_t)grp * p.max_chunks * g + hl) * 2 * 129;
     const int64_t cstride = (int64_t)g * 2 * 129;
     const float* racc = static_cast<const float*>(p.ring_acc);
@@ -76,11 +78,11 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) aacc[k] = use ? racc[cslot * 128 + lane + 32 * k] : 0.f;
     float Mp = NINF, Sp = 0.f, Mb = NINF, Sb = 0.f, ap[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int cb = 0; cb < ch.n; cb += 8) {
+    for (int cb = 0; cb < nsl; cb += 8) {
       float lp[8], lb[8], xp[8][4], xb[8][4];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const bool ok = cb + i < ch.n;
+        const bool ok = cb + i < nsl;
         const float* row = pbase + (int64_t)(cb + i) * cstride;
         lp[i] = ok ? __ldcg(row + 128) : NINF;
         lb[i] = ok ? __ldcg(row + 129 + 128) : NINF;

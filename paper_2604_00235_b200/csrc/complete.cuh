@@ -72,6 +72,10 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
   Chunking ch = group_chunking(p, m, lo_g);
   const int cpos = m - r;
   const int grp = b * Hkv + kvh;
+  {  // the split band's slots come before the plan's (common.cuh band_items)
+    const int pnw = __ldcg(ws_ptr<const int>(p, workspace_layout(p).pn_off) + grp);
+    if (pnw >> 16) ch.n = group_slots(pnw, m, r);
+  }
   const A* pbase = part + ((int64_t)grp * p.max_chunks * g + hl) * 2 * dvp;
   int64_t cstride = (int64_t)g * 2 * dvp;
   if (mode == COMPLETE_SHARDS) {  // one (piece, band) pair per shard, rank order

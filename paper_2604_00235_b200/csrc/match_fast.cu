@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 //      planned by its CTA (or by its last-decided head with PER_HEAD).
 // rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
 template <bool PER_HEAD, int kQDims>
-__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows) {
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb) {
   constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
   constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
   constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
   }
   if (PER_HEAD) {
-    if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos);  // the group's last head plans it
+    if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos, nb);  // the group's last head plans it
     TL_MARK(p, TL_VERIFY_OUT);
     return;
   }
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   if (threadIdx.x == 0) {  // (the amend reads the plan after this grid completes: no fence needed)
     int lo_g = m;
     for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
-    plan_group(p, b, kvh, m, lo_g);
+    plan_group(p, b, kvh, m, lo_g, nb);
   }
   TL_MARK(p, TL_VERIFY_OUT);
 }
@@ -440,11 +440,12 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
   if (qdims == 32)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows);
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -479,21 +480,33 @@ static const FrontVariant kFrontVariants[] = {
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
 // passes: bit 0 = the scan (append, rows), bit 1 = the verify kernel (two-pass mode only)
-cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append,
-                              int rotate_only, int plan, int passes) {
+static int front_variant() {
   static int vi = -1;
   if (vi < 0) {
     const char* env = getenv("MAC_FRONT_VARIANT");
     vi = env ? atoi(env) : 0;
     if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
   }
-  const FrontVariant& v = kFrontVariants[vi];
+  return vi;
+}
+static bool verify_per_group(const MacDecodeParams& p) {
+  return p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
+}
+// whether a match launch of the fast front runs the two-pass scan + verify kernels
+bool front_two_pass(const MacDecodeParams& p) {
+  return match_fast_supported(p) && kFrontVariants[front_variant()].two_pass &&
+         (verify_per_group(p) || p.batch * p.n_q_heads >= 148) && p.window <= 1024;
+}
+
+cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append,
+                              int rotate_only, int plan, int passes) {
+  const FrontVariant& v = kFrontVariants[front_variant()];
   // the two-pass front covers the match stage only: append-only launches use the one-pass kernel,
   // and so does a batch with fewer heads than SMs (one long request): too little verify parallelism
   // verify: a CTA per GQA group when groups fill the SMs, a CTA per head when only heads do
-  const bool per_group = p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
+  const bool per_group = verify_per_group(p);
   const bool per_head = !per_group && p.batch * p.n_q_heads >= 148;
-  const bool two_pass = v.two_pass && do_match && (per_group || per_head) && p.window <= 1024;
+  const bool two_pass = do_match && front_two_pass(p);
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;

@@ -22,6 +22,7 @@ and per engine: page_table [B, pages_per_seq] int32 shared by all layers.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 
@@ -513,7 +514,12 @@ class StepGraph:
     `layer` is one layer index, or a sequence of layers captured back to back in one graph
     (one token of a trace replay across the model: one H2D copy of every
     layer's q/k/v, one launch of the graph, one D2H copy of every layer's output); the host
-    buffers then carry a leading layer dimension in the order given."""
+    buffers then carry a leading layer dimension in the order given.
+
+    The host legs run as kernels on the pinned buffers' device aliases (`mac_io_copy`,
+    csrc/io.cu), not through the copy engines: the inputs are pulled over the host link by
+    one kernel and the output is pushed back by another that narrows it to `out_dtype` on
+    the way (tools/zerocopy_probe.cu: 18 vs 30 us for the two legs at C3)."""
 
     def __init__(self, eng: "BatchDecodeEngine", layer, dtype=torch.bfloat16, out_dtype=None):
         """dtype: the q/k/v input dtype; out_dtype: the host output dtype (default the engine's
@@ -549,11 +555,16 @@ class StepGraph:
                          for i in range(n_l)]
         self.q_dev, self.k_dev, self.v_dev = self._qkv_dev[0]
         self.out_dtype = out_dtype or eng.sumdt
+        if self.out_dtype != eng.sumdt and not (eng.sumdt == torch.float32 and self.out_dtype == torch.bfloat16):
+            raise ValueError(f"StepGraph output {self.out_dtype} from {eng.sumdt} summaries: same dtype or f32 -> bf16")
         oshape = (n_l, B, cfg.n_q_heads, cfg.d_v) if self.multi else (B, cfg.n_q_heads, cfg.d_v)
         self.out_host = torch.zeros(oshape, dtype=self.out_dtype).pin_memory()
-        # a device staging output when the dtype narrows or several layers share the engine's o_out
-        self.out_dev = (torch.zeros(oshape, dtype=self.out_dtype, device=dev)
-                        if (self.out_dtype != eng.sumdt or self.multi) else None)
+        # device aliases of the pinned buffers (UVA): the I/O kernels load / store them directly
+        lib = _lib.load()
+        self._in_alias, self._out_alias = C.c_void_p(), C.c_void_p()
+        _lib.check(lib.mac_host_alias(C.c_void_p(self.in_host.data_ptr()), C.byref(self._in_alias)), "mac_host_alias")
+        _lib.check(lib.mac_host_alias(C.c_void_p(self.out_host.data_ptr()), C.byref(self._out_alias)),
+                   "mac_host_alias")
         self.graph = torch.cuda.CUDAGraph()
         self.h2d_bytes = self.in_host.numel() * self.in_host.element_size()
         self.d2h_bytes = self.out_host.numel() * self.out_host.element_size()
@@ -564,15 +575,26 @@ class StepGraph:
         with torch.cuda.graph(self.graph, stream=s, capture_error_mode="thread_local"):
             self._body()
 
+    def _io(self, src: int, src_dt: int, dst: int, dst_dt: int, n: int):
+        lib = _lib.load()
+        _lib.check(lib.mac_io_copy(C.c_void_p(src), src_dt, C.c_void_p(dst), dst_dt, n,
+                                   C.c_void_p(torch.cuda.current_stream(self.eng.device).cuda_stream)), "mac_io_copy")
+
     def _body(self):
         eng = self.eng
-        self.in_dev.copy_(self.in_host, non_blocking=True)
+        dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16, torch.float64: _lib.DT_F64}
+        self._io(self._in_alias.value, dt[self.in_host.dtype], self.in_dev.data_ptr(), dt[self.in_dev.dtype],
+                 self.in_host.numel())
+        per_out = eng.o_out.numel()
+        osz = self.out_host.element_size()
         for i, lay in enumerate(self.layers):
             q, k, v = self._qkv_dev[i]
             eng.decode_step(lay, q, k, v)
-            if self.out_dev is not None:  # narrowed on the device first: fewer bytes over the host link
-                (self.out_dev[i] if self.multi else self.out_dev).copy_(eng.o_out)
-        self.out_host.copy_(self.out_dev if self.out_dev is not None else eng.o_out, non_blocking=True)
+            if self.multi:  # each layer's output leaves before the next layer reuses o_out
+                self._io(eng.o_out.data_ptr(), dt[eng.o_out.dtype], self._out_alias.value + i * per_out * osz,
+                         dt[self.out_dtype], per_out)
+        if not self.multi:
+            self._io(eng.o_out.data_ptr(), dt[eng.o_out.dtype], self._out_alias.value, dt[self.out_dtype], per_out)
 
     def replay(self):
         self.graph.replay()
