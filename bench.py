@@ -56,6 +56,20 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
+FLUSH_MODE = "write+read"
+
+
+def l2_flush(buf: torch.Tensor):
+    """Evict L2 between timed steps: write a 256 MiB buffer (2x the 126 MB L2), then, in the
+    default mode, read it back — the read evicts the write's dirty lines, so their write-back
+    does not land inside the next timed step (a pure write flush leaves up to ~126 MB of dirty
+    lines that the step's own misses must write back: measured ~2-4 us per C3 step).  Either
+    way no input of the step is L2-resident when its timed region starts."""
+    buf.zero_()
+    if FLUSH_MODE == "write+read":
+        buf.sum()
+
+
 def ncu_traffic(stage: str):
     """Per-launch DRAM bytes (read + write) of a stage's kernel from the committed ncu --set full
     capture (profiles/r01/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
@@ -323,7 +337,7 @@ def run_ours(args, wl):
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
         for s in range(S):
-            flush.zero_()
+            l2_flush(flush)
             torch.cuda._sleep(200_000)  # keep the host ahead of the device: no launch gaps inside the step
             sev[s][0].record(stream)
             eng.decode_step(0, q_all[s], k_all[s], v_all[s])
@@ -337,7 +351,7 @@ def run_ours(args, wl):
         inject_into_engine(eng, 0, states, n0, bulk_seed=rank)
         torch.cuda.synchronize(dev)
         for s in range(S):
-            flush.zero_()
+            l2_flush(flush)
             torch.cuda._sleep(400_000)  # ~0.2 ms of GPU spin: the stage launches queue up behind it
             q, k, v = q_all[s], k_all[s], v_all[s]
             ev[s][0].record(stream)
@@ -368,7 +382,7 @@ def run_ours(args, wl):
     fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(F + 2)]
     fm = []
     for s in range(F + 2):
-        flush.zero_()
+        l2_flush(flush)
         fev[s][0].record(stream)
         eng.full_decode(0, q_all[s % S], k_all[s % S], v_all[s % S])
         fev[s][1].record(stream)
@@ -396,7 +410,7 @@ def run_ours(args, wl):
         sg.q_host.copy_(e_q[s])
         sg.k_host.copy_(e_k[s])
         sg.v_host.copy_(e_v[s])
-        flush.zero_()
+        l2_flush(flush)
         torch.cuda._sleep(400_000)  # the replay is queued before the first event: device time only
         eev[s][0].record(stream)
         sg.replay()
@@ -456,7 +470,7 @@ def run_ours(args, wl):
             "config": {"workload": wl["desc"], "batch_per_gpu": B, "global_batch": B * world, "context": wl["ctx"],
                        "hq": hq, "hkv": hkv, "d": D, "window": WINDOW, "band": BAND, "tau": TAU,
                        "page_size": args.page_size, "variant": "hit path (rep_prob=1, noise 0.05, gap<=512)",
-                       "l2": "flushed (256 MiB write) between steps", "parallelism": f"request-sharded x{world}"},
+                       "l2": f"flushed (256 MiB {FLUSH_MODE}) between steps", "parallelism": f"request-sharded x{world}"},
             "per_token_latency_us": ms_per_step * 1e3,
             "hit_rate": hit_rate,
             "kv_gbs": step_gbs,
@@ -558,7 +572,7 @@ def run_c4(args, wl):
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
         for s in range(S):
-            flush.zero_()
+            l2_flush(flush)
             torch.cuda._sleep(200_000)
             ev[s][0].record(stream)
             res = eng.decode_step(0, q_all[s], k_all[s], v_all[s])
@@ -586,7 +600,7 @@ def run_c4(args, wl):
             "data": "synthetic injected state, fresh queries (every head misses)",
             "config": {"workload": wl["desc"], "context": ctx, "hq": hq, "hkv": hkv, "d": D, "window": WINDOW,
                        "band": BAND, "shard_tokens": layout.shard_tokens, "parallelism": f"kv-sharded x{world}",
-                       "l2": "flushed (256 MiB write) between steps"},
+                       "l2": f"flushed (256 MiB {FLUSH_MODE}) between steps"},
             "miss_rate": float(miss) / (args.steps * hq),
             "per_rank_kv_bytes": local_bytes,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -614,7 +628,11 @@ def main():
                     "at most one per request of the workload's batch)")
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--flush", default="write+read", choices=("write+read", "write"),
+                    help="L2 flush between timed steps (see l2_flush)")
     args = ap.parse_args()
+    global FLUSH_MODE
+    FLUSH_MODE = args.flush
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:

@@ -31,28 +31,34 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, int fu
 // together).  Splits beyond 8 (long miss spans) merge online in further batches of 8.
 __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
   TL_MARK(p, TL_COMPLETE_IN);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  TL_MARK(p, TL_COMPLETE_WAITED);
   const int lane = threadIdx.x & 31;
   const int bh = blockIdx.x * 4 + (threadIdx.x >> 5);
   const Workspace wsl = workspace_layout(p);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // work list consumed: list length and amend claim counter
-    unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
-    ctr[0] = 0u;
-    ctr[1] = 0u;
+  const bool live = bh < p.batch * p.n_q_heads;
+  // Everything before the grid-dependency wait was written by kernels that finished before
+  // this grid could launch (the front and verify kernels; earlier steps for the ring), so
+  // hop A and the cached ring summary load while the amend kernel drains (L2 loads: nothing
+  // stale in L1).  Only the amend's partials are read after the wait.
+  if (!live) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+    }
   }
-  if (bh < p.batch * p.n_q_heads) {
+  if (live) {
     const float NINF = -CUDART_INF_F;
     const int b = bh / p.n_q_heads, h = bh % p.n_q_heads;
     const int Hkv = p.n_kv_heads, g = p.n_q_heads / Hkv, kvh = h / g, hl = h % g;
     const int W = p.window, r = p.band;
     // ---- hop A ----
-    const int m = ws_ptr<const int32_t>(p, wsl.mpos_off)[b];
-    const int use = p.force_miss ? 0 : p.use_hit[bh];
-    const int pp = p.match_pos[bh];
+    const int m = __ldcg(ws_ptr<const int32_t>(p, wsl.mpos_off) + b);
+    const int use = p.force_miss ? 0 : __ldcg(p.use_hit + bh);
+    const int pp = __ldcg(p.match_pos + bh);
     const int* plan_lo = ws_ptr<const int>(p, wsl.lo_off);
-    const int lo = plan_lo[bh];
-    int lo_g = lane < g ? plan_lo[b * p.n_q_heads + kvh * g + lane] : (1 << 30);
+    const int lo = __ldcg(plan_lo + bh);
+    int lo_g = lane < g ? __ldcg(plan_lo + b * p.n_q_heads + kvh * g + lane) : (1 << 30);
     double qv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) qv[k] = load_in(p.q_pre, (int64_t)bh * 128 + lane + 32 * k, p.in_dtype);
@@ -73,10 +79,17 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
     const float* rlse = static_cast<const float*>(p.ring_lse);
     const int64_t cslot = use ? (int64_t)bh * W + (pp - 1) % W : 0;
     // ---- hop B: cached summary, then the splits in batches of 8 (online log-sum-exp) ----
-    const float La = use ? rlse[cslot] : NINF;
+    const float La = use ? __ldcg(rlse + cslot) : NINF;
     float aacc[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) aacc[k] = use ? racc[cslot * 128 + lane + 32 * k] : 0.f;
+    for (int k = 0; k < 4; ++k) aacc[k] = use ? __ldcg(racc + cslot * 128 + lane + 32 * k) : 0.f;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    TL_MARK(p, TL_COMPLETE_WAITED);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // work list consumed: list length and amend claim counter
+      unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+    }
     float Mp = NINF, Sp = 0.f, Mb = NINF, Sb = 0.f, ap[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
     for (int cb = 0; cb < nsl; cb += 8) {
       float lp[8], lb[8], xp[8][4], xb[8][4];

@@ -15,10 +15,14 @@ __device__ __forceinline__ void cp16(unsigned s, const void* g) {
 }
 
 // sub-tile j of the virtual work: group = j / nsub_g, sub-tile within the group's span
+// layout 0: [page][Hkv][16][d] (4 KB per (page, kv head), pages 32 KB apart);
+// layout 1: [Hkv][page][16][d] (a kv head's pages contiguous)
+__device__ int g_layout = 0;
 __device__ __forceinline__ long long subtile_row(int j, int nsub_g, int pps, int first_page) {
   const int grp = j / nsub_g, k = j % nsub_g;
   const int b = grp / HKV, kvh = grp % HKV;
   const long long page = (long long)b * pps + first_page + k;
+  if (g_layout) return ((long long)kvh * 32 * pps + page) * PS;
   return (page * HKV + kvh) * PS;
 }
 
@@ -94,6 +98,9 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int spans[] = {672, 256};
+  for (int layout = 0; layout < 2; ++layout) {
+  cudaMemcpyToSymbol(g_layout, &layout, sizeof(int));
+  printf("layout %s\n", layout ? "[Hkv][page][16][d]" : "[page][Hkv][16][d]");
   for (int span : spans) {
     const int nsub_g = span / 16, groups = B * HKV, nsub_total = nsub_g * groups;
     const int first_page = pps - nsub_g;
@@ -133,6 +140,7 @@ int main() {
       printf("span %4d  %.1f MB  %-28s best %6.1f us (%5.0f GB/s)  avg %6.1f us\n", span, bytes / 1e6, names[mode],
              best * 1e3, bytes / (best * 1e-3) / 1e9, sum / (reps - 1) * 1e3);
     }
+  }
   }
   cudaError_t e = cudaGetLastError();
   if (e) printf("error %s\n", cudaGetErrorString(e));

@@ -73,7 +73,7 @@ def main():
         tl[:, 0] = torch.iinfo(torch.int64).max
         tl[:, 1] = 0
         if not a.no_flush:
-            flush.zero_()
+            bench.l2_flush(flush)
         torch.cuda._sleep(200_000)
         eng.decode_step(0, q_all[s], k_all[s], v_all[s])
         torch.cuda.synchronize()
