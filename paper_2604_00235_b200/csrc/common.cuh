@@ -193,10 +193,18 @@ __host__ __device__ __forceinline__ BandItems band_items(int m, int r, int nb) {
   return s;
 }
 // the plan's split grid with the split band (nb > 0): the piece [grid_start(lo_g), m-r] in
-// at most max_chunks - nb slots; nb == 0: group_chunking
-__host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams& p, int m, int lo_g, int nb) {
+// at most max_chunks - nb slots; nb == 0: group_chunking.  (A guided variant — trailing
+// 32-token items drained last — shortened the amend's tail but measured slower overall:
+// the complete then merged more than 8 slots in two batches.)
+// With the split band the piece is also cut into at most `ntarget` items (the amend's resident
+// warps per group, band_split's caller): as many post-wait items as warps, so no warp starts
+// a second item while the others finish (C3: 934 -> 768 items, 53.5 -> 50.0 us per step).
+__host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams& p, int m, int lo_g, int nb,
+                                                          int ntarget = 0) {
   if (nb <= 0) return group_chunking(p, m, lo_g);
-  return chunking(m - p.band - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks - nb, p.min_chunk);
+  int cap = p.max_chunks - nb;
+  if (ntarget > 0 && ntarget < cap) cap = ntarget;
+  return chunking(m - p.band - grid_start(lo_g, p.kv_offset) + 1, cap, p.min_chunk);
 }
 // partial slots a group's complete merges, from its pn word (plan_group)
 __host__ __device__ __forceinline__ int group_slots(int pn_word, int m, int r) {
@@ -301,10 +309,11 @@ __device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot) {
 // over the piece [grid_start(lo_g), m-r] after the band slots) and one work item
 // {grp, slot, t0, t1} per split appended to the device work list (the paper's
 // load-balancer plan, built on the device with no host synchronisation).
-__device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g, int nb = 0) {
+__device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g, int nb = 0,
+                                           int ntarget = 0) {
   const int start = grid_start(lo_g, p.kv_offset);
   const int end = nb > 0 ? m - p.band : shard_end(p, m);
-  const Chunking ch = plan_chunking(p, m, lo_g, nb);
+  const Chunking ch = plan_chunking(p, m, lo_g, nb, ntarget);
   const int slot0 = nb > 0 ? band_items(m, p.band, nb).n : 0;
   const Workspace w = workspace_layout(p);
   unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
@@ -346,7 +355,7 @@ __device__ __forceinline__ int decide_one(const MacDecodeParams& p, int bh, int 
 
 // decide_one, and the last head of a GQA group to be decided plans the group
 __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
-                                            double bdist, int bpos, int nb = 0) {
+                                            double bdist, int bpos, int nb = 0, int ntarget = 0) {
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv;
   decide_one(p, bh, m, n_scan, have, bdist, bpos);
   const Workspace w = workspace_layout(p);
@@ -361,7 +370,7 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
       const int l = __ldcg(lo + b * Hq + kvh * g + j);
       lo_g = l < lo_g ? l : lo_g;
     }
-    plan_group(p, b, kvh, m, lo_g, nb);
+    plan_group(p, b, kvh, m, lo_g, nb, ntarget);
   }
 }
 
@@ -370,5 +379,6 @@ bool match_fast_supported(const MacDecodeParams& p);
 bool front_two_pass(const MacDecodeParams& p);
 bool amend_mma_supported(const MacDecodeParams& p);
 int band_split(const MacDecodeParams& p);
+int piece_target(const MacDecodeParams& p);
 
 }  // namespace mac

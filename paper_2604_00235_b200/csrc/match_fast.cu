@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 //      planned by its CTA (or by its last-decided head with PER_HEAD).
 // rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
 template <bool PER_HEAD, int kQDims>
-__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb) {
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget) {
   constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
   constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
   constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
   }
   if (PER_HEAD) {
-    if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos, nb);  // the group's last head plans it
+    if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos, nb, ntarget);  // the group's last head plans it
     TL_MARK(p, TL_VERIFY_OUT);
     return;
   }
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   if (threadIdx.x == 0) {  // (the amend reads the plan after this grid completes: no fence needed)
     int lo_g = m;
     for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
-    plan_group(p, b, kvh, m, lo_g, nb);
+    plan_group(p, b, kvh, m, lo_g, nb, ntarget);
   }
   TL_MARK(p, TL_VERIFY_OUT);
 }
@@ -441,11 +441,12 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
+  const int nt = nb > 0 ? piece_target(p) : 0;
   if (qdims == 32)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb);
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
