@@ -141,12 +141,13 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
     """Per-request algorithmic bytes of one MAC step, from the step's device decisions.
 
     use/pos: [B, Hq] arrays; m: [B] positions.  Returns dict of totals over the batch.
-    Two-pass match (default): the scan streams dims 0..31 of every live ring row (the
-    contiguous ring_q32 plane), writes a 4-byte partial per row and a 16-byte summary per
-    64 rows; the verify reads the summaries and the other 96 dims of two candidate rows per
-    head.  Rows that survive the bound (a few near-repeats on the hit path) are not counted
+    Two-pass match (default): the scan streams dims 0..P-1 of every live ring row (the
+    contiguous ring_qp plane, P = MAC_PLANAR_DIMS), writes a 4-byte partial per row and a
+    16-byte summary per 64 rows; the verify reads the summaries and the other d - P dims of
+    two candidate rows per head.  Rows that survive the bound (a few near-repeats on the hit path) are not counted
     (a lower bound: the GB/s derived from it cannot be overstated; ncu's DRAM bytes
     cross-check it in profiles/)."""
+    from paper_2604_00235_b200._lib import PLANAR_DIMS as PD
     g = hq // hkv
     B = use.shape[0]
     match = verify = kv = summ = 0
@@ -154,8 +155,8 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
     for b in range(B):
         live = min(int(m[b]) - 1, window)
         if two_pass:
-            match += hq * (live * 32 * s_ring + window * 4 + n_sum * 16 + d * s_ring)
-            verify += hq * (n_sum * 16 + 2 * (d - 32) * s_ring + d * s_ring)
+            match += hq * (live * PD * s_ring + window * 4 + n_sum * 16 + d * s_ring)
+            verify += hq * (n_sum * 16 + 2 * (d - PD) * s_ring + d * s_ring)
         else:
             match += hq * live * d * s_ring + hq * d * s_ring
         for j in range(hkv):
@@ -164,7 +165,7 @@ def step_bytes(use, pos, m, hq, hkv, d, window, band, s_kv=2, s_ring=2, two_pass
             lo = min((max(1, int(pp) - band + 1) if uu else 1) for uu, pp in zip(u, p))
             kv += (int(m[b]) - lo + 1) * 2 * d * s_kv
         summ += int(use[b].sum()) * (d * 4 + 4)
-    ring_w = B * hq * (d * s_ring + 32 * s_ring + d * 4 + 4)  # ring_q row, its ring_q32 copy, summary
+    ring_w = B * hq * (d * s_ring + PD * s_ring + d * 4 + 4)  # ring_q row, its ring_qp copy, summary
     out_w = B * hq * d * 4
     append = B * hkv * 2 * d * s_kv
     return {"match": match, "verify": verify, "amend": kv, "complete": summ + ring_w + out_w, "append": append,
@@ -373,7 +374,7 @@ def run_ours(args, wl):
     use = use_log.cpu().numpy()
     pos = pos_log.cpu().numpy()
     mm = m_log.cpu().numpy()
-    two_pass = os.environ.get("MAC_FRONT_VARIANT", "0") in ("0", "4", "5")
+    two_pass = os.environ.get("MAC_FRONT_VARIANT", "0") in ("0", "4", "5", "6", "7")
     byts = [step_bytes(use[s], pos[s], mm[s], hq, hkv, D, WINDOW, BAND, two_pass=two_pass) for s in range(W_, S)]
     hit_rate = float(use[W_:].mean())
 
@@ -557,7 +558,7 @@ def run_c4(args, wl):
     e.ring_q[0][0][:, slots_r] = torch.from_numpy(st.ring_q).to(dev, e.sdt)
     e.ring_acc[0][0][:, slots_r] = torch.from_numpy(st.ring_acc).to(dev, e.sumdt)
     e.ring_lse[0][0][:, slots_r] = torch.from_numpy(st.ring_lse).to(dev, e.sumdt)
-    e.sync_ring_q32(0)
+    e.sync_ring_qp(0)
     e.seq_lens[0].fill_(n0)
     bf = torch.bfloat16
     q_all = torch.from_numpy(st.step_q[:, None]).to(dev, bf)

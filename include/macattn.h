@@ -48,7 +48,9 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 4
+#define MACATTN_ABI_VERSION 5
+/* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
+#define MAC_PLANAR_DIMS 16
 
 /* storage modes: dtype of the K/V cache and the query ring; summaries are
  * f32 in MAC_MODE_F32/BF16 and f64 in MAC_MODE_F64 (engine.py:152-153 allows
@@ -108,10 +110,11 @@ typedef struct MacDecodeParams {
   void* ring_q;               /* [B, Hq, W, d]   pre-RoPE queries, storage dtype */
   void* ring_acc;             /* [B, Hq, W, d_v] prefix summary acc (f32 | f64) */
   void* ring_lse;             /* [B, Hq, W]      prefix summary lse (-inf: empty) */
-  void* ring_q32;             /* optional [B, Hq, W, 32] bf16: dims 0..31 of every ring_q row,
-                                 contiguous per head, kept in step by the ring write-back; the
-                                 two-pass scan of the bf16 d = 128 path streams it (NULL: it reads
-                                 the strided row prefixes of ring_q) */
+  void* ring_qp;              /* optional [B, Hq, W, MAC_PLANAR_DIMS] bf16: dims 0..15 of every
+                                 ring_q row, contiguous per head (32 B per row), kept in step by
+                                 the ring write-back; pass 1 of the two-pass scan of the bf16
+                                 d = 128 path streams it (NULL: it reads the strided row prefixes
+                                 of ring_q) */
   const double* rope_freqs;   /* [d/2] omega_j = base^(-2j/d) (attention.py:208-209) */
   /* ---- per-step inputs (device) ---------------------------------------- */
   const void* q_pre;          /* [B, Hq, d]   pre-RoPE queries */

@@ -13,7 +13,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
+PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
@@ -86,7 +87,7 @@ class MacDecodeParams(C.Structure):
         ("ring_q", C.c_void_p),
         ("ring_acc", C.c_void_p),
         ("ring_lse", C.c_void_p),
-        ("ring_q32", C.c_void_p),
+        ("ring_qp", C.c_void_p),
         ("rope_freqs", C.c_void_p),
         ("q_pre", C.c_void_p),
         ("k_pre", C.c_void_p),

@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
     __syncwarp();  // every lane read its cached slice above, before this slot can be overwritten
 #pragma unroll
     for (int k = 0; k < 4; ++k) rq[wslot * 128 + lane + 32 * k] = from_f64<__nv_bfloat16>(qv[k]);
-    if (p.ring_q32) static_cast<__nv_bfloat16*>(p.ring_q32)[wslot * 32 + lane] = from_f64<__nv_bfloat16>(qv[0]);
+    if (p.ring_qp && lane < MAC_PLANAR_DIMS)  // the scan's planar copy of dims 0..P-1
+      static_cast<__nv_bfloat16*>(p.ring_qp)[wslot * MAC_PLANAR_DIMS + lane] = from_f64<__nv_bfloat16>(qv[0]);
     if (lane == 0) {
       if (p.cached_lse) static_cast<float*>(p.cached_lse)[bh] = La;
       if (h == 0) p.seq_lens[b] = m;

@@ -228,8 +228,8 @@ __device__ __forceinline__ void complete_head(const MacDecodeParams& p, int bh, 
       const int e = lane + 32 * k;
       if (e < d) rq[wslot * d + e] = from_f64<kv_t>(qv[k]);
     }
-    if (MODE == MAC_MODE_BF16 && d == 128 && p.ring_q32)  // the scan's contiguous dims-0..31 copy
-      static_cast<kv_t*>(p.ring_q32)[wslot * 32 + lane] = from_f64<kv_t>(qv[0]);
+    if (MODE == MAC_MODE_BF16 && d == 128 && p.ring_qp && lane < MAC_PLANAR_DIMS)  // the scan's planar copy
+      static_cast<kv_t*>(p.ring_qp)[wslot * MAC_PLANAR_DIMS + lane] = from_f64<kv_t>(qv[0]);
     for (int e = lane + 32 * kElems; e < d; e += 32)  // d > 128
       rq[wslot * d + e] = from_f64<kv_t>(load_in(p.q_pre, (int64_t)bh * d + e, p.in_dtype));
   }

@@ -156,8 +156,8 @@ __device__ __forceinline__ float dist8_f2(const unsigned long long* q2, uint4 c)
 // ring bytes; when nearly every row survives (a fresh query, all distances
 // ~2d) pass 2 reads the second halves of all rows — the one-pass bytes.  The
 // distance is the one-pass kernel's fp32 sum of squares split in two sums.
-// PLANAR (kQDims = 32): the rows are read from ring_q32, 64 contiguous bytes per row
-// (a contiguous 64 KiB stream per head) instead of the strided 64-byte prefixes of ring_q.
+// PLANAR (kQDims = MAC_PLANAR_DIMS = 16): the rows are read from ring_qp, 32 contiguous bytes
+// per row (a contiguous 32 KiB stream per head) instead of strided prefixes of ring_q.
 template <int kRowsPerCta, int kMinBlocks, int kQDims, bool PLANAR = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDecodeParams p, int n_match,
                                                                           int do_append, int rotate_only, int plan,
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   constexpr int LPR = kQDims / 8;                    // lanes per row (16 B = 8 dims each)
   constexpr int RPW = 32 / LPR;                      // rows per warp-load
   constexpr int kLoads = kRowsPerCta / (8 * RPW);    // loads per lane
-  static_assert(kLoads >= LPR && kLoads % LPR == 0 && (LPR == 8 || LPR == 4), "reduce-scatter layout");
+  static_assert(kLoads >= LPR && kLoads % LPR == 0 && (LPR == 8 || LPR == 4 || LPR == 2), "reduce-scatter layout");
   constexpr int NF = kLoads / LPR;                   // rows each lane ends up holding
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   const int b = bh / p.n_q_heads;
   const int m = p.seq_lens[b] + 1;
   const int sub = lane % LPR, quad = lane / LPR;
-  static_assert(!PLANAR || kQDims == 32, "ring_q32 holds 32 dims");
-  constexpr int kRowU4 = PLANAR ? 4 : 16;  // uint4 per row of the source
-  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(PLANAR ? p.ring_q32 : p.ring_q) +
+  static_assert(!PLANAR || kQDims == MAC_PLANAR_DIMS, "ring_qp holds MAC_PLANAR_DIMS dims");
+  constexpr int kRowU4 = PLANAR ? kQDims / 8 : 16;  // uint4 per row of the source
+  const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(PLANAR ? p.ring_qp : p.ring_q) +
                                                      (int64_t)bh * W * (kRowU4 * 8));
   const int row0 = split * kRowsPerCta;
   uint4 v[kLoads];
@@ -442,6 +442,9 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   cfg.numAttrs = 1;
   const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
   const int nt = nb > 0 ? piece_target(p) : 0;
+  if (qdims == 16)
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt);
   if (qdims == 32)
     return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt)
                     : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt);
@@ -457,7 +460,7 @@ bool front_fast_supported(const MacDecodeParams& p) {
 }
 
 // MAC_FRONT_VARIANT (development knob): two-pass match, (ring rows per CTA, min CTAs per SM,
-// first-pass dims) = 0: (512, 4, 32) default, reading ring_q32 when given; 4: (256, 4, 64) on
+// first-pass dims) = 0: (512, 4, 16) default, reading ring_qp when given; 6: (512, 4, 32); 4: (256, 4, 64) on
 // ring_q; 5: (256, 4, 32); one-pass stream 1-3: (128,5), (64,8), (256,3).  C3 step (us):
 // 59.8 (0), 67.8 (4); the (256,6) and (512,3) shapes scanned 3.5 and 0.8 us slower than (0).
 // Measured alternatives that lost on C3 (persistent tensor-core, persistent CUDA-core, f32x2
@@ -468,15 +471,17 @@ struct FrontVariant {
   int rows;
   bool two_pass;  // front_half_kernel + verify_kernel
   int qdims;      // dims of the first pass (two-pass)
-  void (*fn_planar)(MacDecodeParams, int, int, int, int, int);  // reads ring_q32 when it is given
+  void (*fn_planar)(MacDecodeParams, int, int, int, int, int);  // reads ring_qp when it is given
 };
 static const FrontVariant kFrontVariants[] = {
-    {front_half_kernel<512, 4, 32>, 512, true, 32, front_half_kernel<512, 4, 32, true>},
+    {front_half_kernel<512, 4, 16>, 512, true, 16, front_half_kernel<512, 4, 16, true>},
     {front_bf16_d128_kernel<128, 5>, 128, false, 0, nullptr},
     {front_bf16_d128_kernel<64, 8>, 64, false, 0, nullptr},
     {front_bf16_d128_kernel<256, 3>, 256, false, 0, nullptr},
     {front_half_kernel<256, 4, 64>, 256, true, 64, nullptr},
-    {front_half_kernel<256, 4, 32>, 256, true, 32, front_half_kernel<256, 4, 32, true>},
+    {front_half_kernel<256, 4, 32>, 256, true, 32, nullptr},
+    {front_half_kernel<512, 4, 32>, 512, true, 32, nullptr},
+    {front_half_kernel<1024, 4, 16>, 1024, true, 16, front_half_kernel<1024, 4, 16, true>},
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
@@ -513,7 +518,7 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0) return cudaSuccess;
   if (passes & 1) {
-    auto fn = (do_match && u.fn_planar && p.ring_q32) ? u.fn_planar : u.fn;
+    auto fn = (do_match && u.fn_planar && p.ring_qp) ? u.fn_planar : u.fn;
     fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;

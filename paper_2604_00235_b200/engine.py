@@ -164,9 +164,10 @@ class BatchDecodeEngine:
         self.ring_q = [torch.zeros(B, Hq, W, d, dtype=self.sdt, device=dev) for _ in range(L)]
         self.ring_acc = [torch.zeros(B, Hq, W, dv, dtype=self.sumdt, device=dev) for _ in range(L)]
         self.ring_lse = [torch.full((B, Hq, W), -math.inf, dtype=self.sumdt, device=dev) for _ in range(L)]
-        # bf16 d = 128: dims 0..31 of every ring row, contiguous per head, for the two-pass scan
-        # (kept in step by the ring write-back; call sync_ring_q32 after writing ring_q directly)
-        self.ring_q32 = ([torch.zeros(B, Hq, W, 32, dtype=self.sdt, device=dev) for _ in range(L)]
+        # bf16 d = 128: dims 0..PLANAR_DIMS-1 of every ring row, contiguous per head, for pass 1
+        # of the two-pass scan (kept in step by the ring write-back; call sync_ring_qp after
+        # writing ring_q directly)
+        self.ring_qp = ([torch.zeros(B, Hq, W, _lib.PLANAR_DIMS, dtype=self.sdt, device=dev) for _ in range(L)]
                          if cfg.storage == "bf16" and cfg.d == 128 else None)
         self.seq_lens = [torch.zeros(B, dtype=torch.int32, device=dev) for _ in range(L)]
         i32 = dict(dtype=torch.int32, device=dev)
@@ -275,7 +276,7 @@ class BatchDecodeEngine:
         P.ring_q = self.ring_q[layer].data_ptr()
         P.ring_acc = self.ring_acc[layer].data_ptr()
         P.ring_lse = self.ring_lse[layer].data_ptr()
-        P.ring_q32 = self.ring_q32[layer].data_ptr() if self.ring_q32 is not None else None
+        P.ring_qp = self.ring_qp[layer].data_ptr() if self.ring_qp is not None else None
         P.rope_freqs = self.freqs.data_ptr()
         P.q_pre, P.k_pre, P.v_in = q.data_ptr(), k.data_ptr(), v.data_ptr()
         P.out = self.o_out.data_ptr()
@@ -494,13 +495,13 @@ class BatchDecodeEngine:
         self.ring_acc[layer][:, :, slots] = ring_acc.to(self.device, self.sumdt)
         self.ring_lse[layer][:, :, slots] = ring_lse.to(self.device, self.sumdt)
         self.seq_lens[layer].fill_(L)
-        self.sync_ring_q32(layer)
+        self.sync_ring_qp(layer)
 
-    def sync_ring_q32(self, layer: int):
-        """Refresh the contiguous dims-0..31 copy of the query ring after ring_q was written
-        from outside the kernels (state injection)."""
-        if self.ring_q32 is not None:
-            self.ring_q32[layer].copy_(self.ring_q[layer][..., :32])
+    def sync_ring_qp(self, layer: int):
+        """Refresh the planar copy of the query ring's first PLANAR_DIMS dims after ring_q was
+        written from outside the kernels (state injection)."""
+        if self.ring_qp is not None:
+            self.ring_qp[layer].copy_(self.ring_q[layer][..., :_lib.PLANAR_DIMS])
 
 
 class StepGraph:

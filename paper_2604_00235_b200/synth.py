@@ -108,7 +108,7 @@ def inject_into_engine(eng, layer: int, states: list, n0: int, *, bulk_seed: int
         eng.ring_q[layer][b][:, slots_r] = torch.from_numpy(st.ring_q).to(dev, eng.sdt)
         eng.ring_acc[layer][b][:, slots_r] = torch.from_numpy(st.ring_acc).to(dev, eng.sumdt)
         eng.ring_lse[layer][b][:, slots_r] = torch.from_numpy(st.ring_lse).to(dev, eng.sumdt)
-    eng.sync_ring_q32(layer)
+    eng.sync_ring_qp(layer)
     eng.seq_lens[layer].fill_(n0)
 
 

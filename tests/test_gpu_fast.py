@@ -67,7 +67,7 @@ def test_fast_replay_matches_oracle(hq, hkv, window, band, delta_max):
 @pytest.mark.parametrize("downdate", ["split", "remove"])
 def test_fast_ring_state_and_downdate(downdate):
     """The decode step's complete on the bf16 path (complete_bf16_kernel): outputs, band mass,
-    the ring summary written at slot (m-1) % W and the ring_q32 copy, with the split prefix
+    the ring summary written at slot (m-1) % W and the planar ring_qp copy, with the split prefix
     and with the remove() downdate (engine.py:474-478), against the oracle every step."""
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
 
@@ -111,7 +111,8 @@ def test_fast_ring_state_and_downdate(downdate):
     # cancellation amplifies rounding, and reused prefixes carry it into later outputs
     assert worst_out <= (TOL if downdate == "split" else 1e-3), worst_out
     assert worst_ring <= 1e-3 and worst_lse <= 1e-3, (worst_ring, worst_lse)
-    assert torch.equal(eng.ring_q32[0], eng.ring_q[0][..., :32])
+    from paper_2604_00235_b200._lib import PLANAR_DIMS
+    assert torch.equal(eng.ring_qp[0], eng.ring_q[0][..., :PLANAR_DIMS])
 
 
 def test_fast_long_context_hits_and_misses():
@@ -339,5 +340,6 @@ def test_two_pass_match_large_batch_replay(B, hq, hkv):
                     worst = max(worst, rel_err(go[b, h], st.outputs[h]))
     assert hits > 0 and misses > 0
     assert worst <= TOL, worst
-    # the scan's contiguous dims-0..31 copy of the ring follows every write-back
-    assert torch.equal(eng.ring_q32[0], eng.ring_q[0][..., :32])
+    # the scan's contiguous planar copy of the ring follows every write-back
+    from paper_2604_00235_b200._lib import PLANAR_DIMS
+    assert torch.equal(eng.ring_qp[0], eng.ring_q[0][..., :PLANAR_DIMS])
