@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 5
+#define MACATTN_ABI_VERSION 6
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -132,6 +132,9 @@ typedef struct MacDecodeParams {
   void* cached_acc;           /* optional [B, Hq, d_v]: summary reused at p (NULL: not written) */
   void* cached_lse;           /* optional [B, Hq] */
   int32_t* fallbacks;         /* optional [B, Hq]: 1 when remove() fell back to the split prefix */
+  void* out_bf16;             /* optional [B, Hq, d_v] bf16: the output narrowed, written by the bf16
+                                 d = 128 complete beside `out` — e.g. the device alias of a pinned
+                                 host buffer, so the step's result reaches the host with no copy */
   /* ---- KV-sharded miss path ------------------------------ */
   void* shard_out;            /* [B, Hq, 2, d_v+1] this shard's (piece, band) partials: acc..., lse */
   const void* shard_parts;    /* [n_shards, B, Hq, 2, d_v+1] every shard's partials, rank order */

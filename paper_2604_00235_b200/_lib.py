@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -103,6 +103,7 @@ class MacDecodeParams(C.Structure):
         ("cached_acc", C.c_void_p),
         ("cached_lse", C.c_void_p),
         ("fallbacks", C.c_void_p),
+        ("out_bf16", C.c_void_p),
         ("shard_out", C.c_void_p),
         ("shard_parts", C.c_void_p),
         ("workspace", C.c_void_p),

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
         const T pre = (dLa == TINF) ? pk : (dLp == TINF ? (T)aacc[k] : aacc[k] * wa + pk * wp);
         const T full = (Lpre == TINF) ? bk : (dLb == TINF ? pre : pre * wpre + bk * wb);
         out[(int64_t)bh * 128 + e] = (float)full;
+        if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[(int64_t)bh * 128 + e] = __float2bfloat16_rn((float)full);
         if (p.cached_acc) static_cast<float*>(p.cached_acc)[(int64_t)bh * 128 + e] = aacc[k];
         racc_w[wslot * 128 + e] = (float)(do_remove ? ((Lrem == TINF) ? zero : full * wr_full - bk * wr_band) : pre);
       }

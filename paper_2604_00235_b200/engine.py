@@ -107,6 +107,16 @@ def default_max_chunks(batch: int, n_kv_heads: int, max_seq_len: int = 0) -> int
     return int(min(2048, max(8, math.ceil(SM_COUNT_B200 * 6 * 2 / groups), math.ceil(max_seq_len / 8192))))
 
 
+class _Ptr:
+    """A raw device address where _params expects a tensor."""
+
+    def __init__(self, ptr: int):
+        self._p = int(ptr)
+
+    def data_ptr(self) -> int:
+        return self._p
+
+
 @dataclass
 class BatchStepResult:
     """Device tensors of one batched step (views of engine-owned buffers; valid until the next step)."""
@@ -330,6 +340,15 @@ class BatchDecodeEngine:
             self._accumulate_stats(layer, P)
         return self.result()
 
+    def _decode_step_ptrs(self, layer: int, q_ptr: int, k_ptr: int, v_ptr: int, in_dt: int, out_bf16: int = 0):
+        """decode_step on raw device pointers, optionally also writing the output narrowed to
+        bf16 at `out_bf16` (a pinned host buffer's device alias: StepGraph's zero-copy output)."""
+        P = self._params(layer, _Ptr(q_ptr), _Ptr(k_ptr), _Ptr(v_ptr), in_dt, False)
+        P.out_bf16 = out_bf16 or None
+        _lib.call("mac_decode_step", P, self._stream())
+        if self.track_stats and not getattr(self, "_in_prefill", False):
+            self._accumulate_stats(layer, P)
+
     # ------------------------------------------------------------------ diagnostics
     def _accumulate_stats(self, layer: int, P):
         code = _lib.load().mac_step_stats(P, C_void(self.head_stats[layer].data_ptr()),
@@ -517,10 +536,13 @@ class StepGraph:
     layer's q/k/v, one launch of the graph, one D2H copy of every layer's output); the host
     buffers then carry a leading layer dimension in the order given.
 
-    The host legs run as kernels on the pinned buffers' device aliases (`mac_io_copy`,
-    csrc/io.cu), not through the copy engines: the inputs are pulled over the host link by
-    one kernel and the output is pushed back by another that narrows it to `out_dtype` on
-    the way (tools/zerocopy_probe.cu: 18 vs 30 us for the two legs at C3)."""
+    The host legs never use the copy engines: the inputs are pulled over the host link by a
+    zero-copy kernel on the pinned buffer's device alias (`mac_io_copy`, csrc/io.cu; 18 vs
+    30 us for the two legs at C3 in tools/zerocopy_probe.cu), and on the bf16 d = 128 path
+    with a bf16 output (the serving configuration) the complete kernel writes the narrowed
+    output straight into the pinned output buffer (`out_bf16`); otherwise a second zero-copy
+    kernel pushes it.  (Letting the front kernel read q/k/v from the host alias directly,
+    with no pull launch, measured slower: every scan CTA then waits on a host-link read.)"""
 
     def __init__(self, eng: "BatchDecodeEngine", layer, dtype=torch.bfloat16, out_dtype=None):
         """dtype: the q/k/v input dtype; out_dtype: the host output dtype (default the engine's
@@ -566,6 +588,9 @@ class StepGraph:
         _lib.check(lib.mac_host_alias(C.c_void_p(self.in_host.data_ptr()), C.byref(self._in_alias)), "mac_host_alias")
         _lib.check(lib.mac_host_alias(C.c_void_p(self.out_host.data_ptr()), C.byref(self._out_alias)),
                    "mac_host_alias")
+        # bf16 d = 128 engine with a bf16 output: no I/O kernels at all (see _body)
+        self.direct = (cfg.storage == "bf16" and cfg.d == 128 and cfg.d_v == 128 and
+                       self.out_dtype == torch.bfloat16)
         self.graph = torch.cuda.CUDAGraph()
         self.h2d_bytes = self.in_host.numel() * self.in_host.element_size()
         self.d2h_bytes = self.out_host.numel() * self.out_host.element_size()
@@ -584,10 +609,20 @@ class StepGraph:
     def _body(self):
         eng = self.eng
         dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16, torch.float64: _lib.DT_F64}
-        self._io(self._in_alias.value, dt[self.in_host.dtype], self.in_dev.data_ptr(), dt[self.in_dev.dtype],
-                 self.in_host.numel())
         per_out = eng.o_out.numel()
         osz = self.out_host.element_size()
+        if self.direct:
+            # inputs pulled by one zero-copy kernel; the complete kernel writes the bf16 output
+            # straight into the pinned output buffer (no output launch)
+            self._io(self._in_alias.value, dt[self.in_host.dtype], self.in_dev.data_ptr(), dt[self.in_dev.dtype],
+                     self.in_host.numel())
+            for i, lay in enumerate(self.layers):
+                q, k, v = self._qkv_dev[i]
+                eng._decode_step_ptrs(lay, q.data_ptr(), k.data_ptr(), v.data_ptr(), dt[q.dtype],
+                                      self._out_alias.value + i * per_out * osz)
+            return
+        self._io(self._in_alias.value, dt[self.in_host.dtype], self.in_dev.data_ptr(), dt[self.in_dev.dtype],
+                 self.in_host.numel())
         for i, lay in enumerate(self.layers):
             q, k, v = self._qkv_dev[i]
             eng.decode_step(lay, q, k, v)
