@@ -27,6 +27,10 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
   __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);
   __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(p.v_cache);
   float* qrot = ws_ptr<float>(p, w.qrot_off);
+  // bf16 / f32 inputs (exact in fp32 registers): each head's query pair used to be loaded after
+  // the previous head's store — a memory round trip per head, which made the append warps, not
+  // the scan, end the front kernel (C2: the verify waited 6.7 us past the last scan CTA)
+  const bool batch = p.in_dtype != MAC_DT_F64;
   for (int j = lane; j < 64; j += 32) {
     double s, c;
     sincos((double)m * p.rope_freqs[j], &s, &c);
@@ -38,10 +42,29 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
       kk.y = from_f64<__nv_bfloat16>(x0 * s + x1 * c);
       reinterpret_cast<__nv_bfloat162*>(kc + row * 128)[j] = kk;
     }
-    for (int hl = 0; hl < g; ++hl) {
-      const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
-      const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
-      reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+    if (batch) {  // four heads' query pairs in flight together, then their stores
+      for (int h0 = 0; h0 < g; h0 += 4) {
+        float xa[4], xb[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
+          xa[t] = h0 + t < g ? (float)load_in(p.q_pre, qi, p.in_dtype) : 0.f;
+          xb[t] = h0 + t < g ? (float)load_in(p.q_pre, qi + 1, p.in_dtype) : 0.f;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (h0 + t >= g) break;
+          const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
+          const double x0 = xa[t], x1 = xb[t];
+          reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+        }
+      }
+    } else {
+      for (int hl = 0; hl < g; ++hl) {
+        const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
+        const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
+        reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+      }
     }
   }
   if (store)
