@@ -498,10 +498,13 @@ static int front_variant() {
 static bool verify_per_group(const MacDecodeParams& p) {
   return p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
 }
-// whether a match launch of the fast front runs the two-pass scan + verify kernels
+// whether a match launch of the fast front runs the two-pass scan + verify kernels: enough heads
+// to fill the SMs, and a ring of 512..1024 rows — on smaller rings the one-pass scan reads little
+// more and a head whose query has no near-repeat (every row survives pass 1) costs the verify a
+// chain of round trips (C5 sweep, batch 16, W = 256: 111 us per step two-pass vs 44 one-pass)
 bool front_two_pass(const MacDecodeParams& p) {
   return match_fast_supported(p) && kFrontVariants[front_variant()].two_pass &&
-         (verify_per_group(p) || p.batch * p.n_q_heads >= 148) && p.window <= 1024;
+         (verify_per_group(p) || p.batch * p.n_q_heads >= 148) && p.window >= 512 && p.window <= 1024;
 }
 
 cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do_match, bool do_append,

@@ -307,12 +307,12 @@ def test_step_graph_across_layers():
 
 @pytest.mark.parametrize("B,hq,hkv", [(37, 16, 4), (10, 16, 2)])
 def test_two_pass_match_large_batch_replay(B, hq, hkv):
-    """Enough heads for the two-pass match (first-half scan + verify): one verify CTA per GQA
-    group (B * Hkv >= 148) or per head (fewer groups, B * Hq >= 148); decisions identical
-    and outputs within tolerance of the oracle, hits and misses mixed."""
+    """Enough heads for the two-pass match (planar 16-dim scan + verify; rings of W >= 512): one
+    verify CTA per GQA group (B * Hkv >= 148) or per head (fewer groups, B * Hq >= 148);
+    decisions identical and outputs within tolerance of the oracle, hits and misses mixed."""
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
 
-    L, W, r = 120, 64, 16
+    L, W, r = 120, 512, 16
     trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=300 + s,
                                        rep_prob=0.7)) for s in range(B)]
     cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
