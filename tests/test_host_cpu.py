@@ -178,3 +178,46 @@ def test_diagnostic_entry_points_validate_without_gpu():
     assert lib.mac_mass_bound(p, mb, None) == 1001  # no cache
     p.head_dim = 512
     assert lib.mac_mass_bound(p, mb, None) == 1002  # d > 256
+
+
+def test_io_entry_points_validate_without_gpu():
+    """mac_io_copy / mac_host_alias (StepGraph's zero-copy I/O) reject bad arguments before any
+    launch; the planar ring width of the Python mirror follows the header."""
+    import ctypes
+
+    from paper_2604_00235_b200 import _lib
+
+    lib = _lib.load()
+    out = ctypes.c_void_p()
+    assert lib.mac_host_alias(None, ctypes.byref(out)) == 1001
+    buf = (ctypes.c_uint8 * 64)()
+    base = ctypes.addressof(buf)
+    aligned = base + (-base) % 16
+    assert lib.mac_io_copy(None, _lib.DT_F32, aligned, _lib.DT_F32, 4, None) == 1001
+    assert lib.mac_io_copy(aligned + 4, _lib.DT_F32, aligned, _lib.DT_F32, 4, None) == 1002  # misaligned
+    assert lib.mac_io_copy(aligned, _lib.DT_F32, aligned, _lib.DT_F32, 3, None) == 1002  # 12 bytes
+    assert lib.mac_io_copy(aligned, _lib.DT_F64, aligned, _lib.DT_BF16, 8, None) == 1003  # no f64 -> bf16
+    with open(os.path.join(ROOT, "include", "macattn.h")) as fh:
+        src = fh.read()
+    assert int(re.search(r"#define MAC_PLANAR_DIMS (\d+)", src).group(1)) == _lib.PLANAR_DIMS
+    assert int(re.search(r"#define MACATTN_ABI_VERSION (\d+)", src).group(1)) == _lib.ABI_VERSION
+
+
+def test_ncu_traffic_summary_matches_committed_capture():
+    """profiles/r01/ncu_traffic.json (the bench's roofline.traffic) is what tools/ncu_traffic.py
+    derives from the committed ncu capture of the decode step."""
+    import json
+    import subprocess
+    import sys
+
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_traffic.py"),
+                          os.path.join(ROOT, "profiles", "r01", "ncu_kernels.csv")],
+                         capture_output=True, text=True, check=True)
+    got = json.loads(res.stdout)
+    with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as fh:
+        want = json.load(fh)
+    for stage in ("mac_match_scan", "mac_match_verify", "mac_amend", "mac_complete"):
+        assert got[stage]["traffic_bytes"] == want[stage]["traffic_bytes"], stage
+        assert got[stage]["kernel"] == want[stage]["kernel"], stage
+    # the dominant kernel moves at least its algorithmic bytes and no more than 10 % on top
+    assert 87.1e6 <= want["mac_amend"]["traffic_bytes"] <= 1.1 * 87.1e6
