@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--max-chunks", type=int, default=0)
     ap.add_argument("--min-chunk", type=int, default=128)
+    ap.add_argument("--fresh", action="store_true", help="random queries: every head misses")
     a = ap.parse_args()
     import bench
 
@@ -61,6 +62,9 @@ def main():
     q_all = torch.from_numpy(np.stack([s.step_q for s in states], 1)).to(dev, bf)
     k_all = torch.from_numpy(np.stack([s.step_k for s in states], 1)).to(dev, bf)
     v_all = torch.from_numpy(np.stack([s.step_v for s in states], 1)).to(dev, bf)
+    if a.fresh:
+        gen = torch.Generator(device=dev).manual_seed(7)
+        q_all = torch.randn(q_all.shape, device=dev, generator=gen).to(bf)
     P = eng._params(0, q_all[0], k_all[0], v_all[0], _lib.DT_BF16)
     off = int(lib.mac_timeline_offset(P))
     tl = eng.workspace[off:off + 16 * 16].view(torch.int64).view(16, 2)
