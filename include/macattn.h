@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 6
+#define MACATTN_ABI_VERSION 7
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -141,6 +141,14 @@ typedef struct MacDecodeParams {
   /* ---- scratch --------------------------------------------------------- */
   void* workspace;
   size_t workspace_bytes;
+  /* ---- match-scan choice (bf16 d = 128 path) ------------------------------ */
+  int32_t match_mode;         /* 0: by geometry (two-pass scan + verify for rings of 512..1024 rows
+                                 and enough heads); 1: one-pass scan.  Both are exact: the choice
+                                 never changes a result, only the cost of a miss-heavy step */
+  int32_t* feedback;          /* optional int32[2] (e.g. a pinned host buffer's device alias):
+                                 {heads that missed, heads} over the steps since the last
+                                 publication, stored at the start of every 8th step (the complete
+                                 kernel counts, the append warps publish) */
 } MacDecodeParams;
 
 /* Per-shard (acc, lse) partial merge for the KV-sharded miss path. */

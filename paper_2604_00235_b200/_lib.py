@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -108,6 +108,8 @@ class MacDecodeParams(C.Structure):
         ("shard_parts", C.c_void_p),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
+        ("match_mode", C.c_int32),
+        ("feedback", C.c_void_p),
     ]
 
 

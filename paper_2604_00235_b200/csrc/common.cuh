@@ -239,6 +239,8 @@ struct Workspace {
   size_t marr_off;   // [B*Hq] u32   ring rows scanned so far this step
   size_t gcnt_off;   // [B*Hkv] u32  heads of the group decided so far
   size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter (both reset by complete),
+                     //              4 heads missed and 6 steps completed since the feedback was last published
+                     //              (complete adds; every 8th step's append warps publish and reset)
                      //              (2-15 spare)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  piece splits planned for the group | band items requested << 16

@@ -20,6 +20,15 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
   const Workspace w = workspace_layout(p);
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
   if (lane == 0) ws_ptr<int>(p, w.mpos_off)[b] = m;  // every group's warp (same value)
+  // every 8th step: the misses counted since the last publication (complete.cu) -> host.  Not
+  // every step: a kernel that stores to host memory pays for the flush when it ends (~1 us).
+  if (idx == 0 && lane == 0 && p.feedback && (m & 7) == 0) {
+    unsigned* ctr = ws_ptr<unsigned>(p, w.ctr_off);
+    p.feedback[0] = (int)ctr[4];
+    p.feedback[1] = (int)ctr[6] * p.batch * p.n_q_heads;
+    ctr[4] = 0u;
+    ctr[6] = 0u;
+  }
   const int t_local = m - p.kv_offset;
   const bool store = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
   int64_t row = 0;

@@ -537,7 +537,7 @@ static bool verify_per_group(const MacDecodeParams& p) {
 // more and a head whose query has no near-repeat (every row survives pass 1) costs the verify a
 // chain of round trips (C5 sweep, batch 16, W = 256: 111 us per step two-pass vs 44 one-pass)
 bool front_two_pass(const MacDecodeParams& p) {
-  return match_fast_supported(p) && kFrontVariants[front_variant()].two_pass &&
+  return p.match_mode != 1 && match_fast_supported(p) && kFrontVariants[front_variant()].two_pass &&
          (verify_per_group(p) || p.batch * p.n_q_heads >= 148) && p.window >= 512 && p.window <= 1024;
 }
 

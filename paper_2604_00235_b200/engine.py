@@ -190,6 +190,20 @@ class BatchDecodeEngine:
         self.o_full_lse = torch.zeros(B, Hq, dtype=self.sumdt, device=dev)
         self.o_band_mass = torch.zeros(B, Hq, dtype=self.sumdt, device=dev)
         self.o_fallbacks = torch.zeros(B, Hq, **i32)
+        # Match-scan choice: every 8th step the kernels store {heads that missed, heads} since
+        # the last publication into this pinned buffer through its device alias; the engine
+        # reads it WITHOUT a synchronisation (so it may be ~8-16 steps old) and switch to the one-pass scan while
+        # most heads miss — the two-pass match is built for the hit path.  Both
+        # scans are exact, so a stale choice only costs time.  match_mode="two_pass" /
+        # "one_pass" pin it (tests, profiling); "adaptive" is the default.
+        self.match_mode = "adaptive"
+        self._fb_host = self._fb_alias = None
+        if dev.type == "cuda":
+            self._fb_host = torch.zeros(2, dtype=torch.int32).pin_memory()
+            self._fb_alias = C.c_void_p()
+            _lib.check(_lib.load().mac_host_alias(C.c_void_p(self._fb_host.data_ptr()), C.byref(self._fb_alias)),
+                       "mac_host_alias")
+        self._step_mode = 0
         self.o_cached_acc = torch.zeros(B, Hq, dv, dtype=self.sumdt, device=dev) if record_cached else None
         self.o_cached_lse = torch.zeros(B, Hq, dtype=self.sumdt, device=dev) if record_cached else None
         # KV-sharded path (n_shards >= 1, sharded.py): this shard's (piece, band) summaries and
@@ -297,6 +311,8 @@ class BatchDecodeEngine:
         P.cached_acc = self.o_cached_acc.data_ptr() if self.o_cached_acc is not None else None
         P.cached_lse = self.o_cached_lse.data_ptr() if self.o_cached_lse is not None else None
         P.fallbacks = self.o_fallbacks.data_ptr()
+        P.match_mode = self._step_mode
+        P.feedback = self._fb_alias.value if self._fb_alias is not None else None
         if hasattr(self, "workspace"):
             P.workspace = self.workspace.data_ptr()
             P.workspace_bytes = self.workspace.numel()
@@ -334,6 +350,7 @@ class BatchDecodeEngine:
         refresh gate does (engine.py:456-459)."""
         self._layer(layer)
         dt = self._check_inputs(q_pre, k_pre, v)
+        self._choose_match_mode()
         P = self._params(layer, q_pre, k_pre, v, dt, force_miss)
         _lib.call("mac_decode_step", P, self._stream())
         if self.track_stats and not getattr(self, "_in_prefill", False):
@@ -343,6 +360,7 @@ class BatchDecodeEngine:
     def _decode_step_ptrs(self, layer: int, q_ptr: int, k_ptr: int, v_ptr: int, in_dt: int, out_bf16: int = 0):
         """decode_step on raw device pointers, optionally also writing the output narrowed to
         bf16 at `out_bf16` (a pinned host buffer's device alias: StepGraph's zero-copy output)."""
+        self._choose_match_mode()
         P = self._params(layer, _Ptr(q_ptr), _Ptr(k_ptr), _Ptr(v_ptr), in_dt, False)
         P.out_bf16 = out_bf16 or None
         _lib.call("mac_decode_step", P, self._stream())
@@ -460,9 +478,21 @@ class BatchDecodeEngine:
             self._in_prefill = False
         return res
 
+    def _choose_match_mode(self):
+        """The step's match scan (MacDecodeParams.match_mode), fixed for all of its stages."""
+        if self.match_mode == "one_pass":
+            self._step_mode = 1
+        elif self.match_mode == "two_pass" or self._fb_host is None:
+            self._step_mode = 0
+        else:
+            missed, heads = (int(x) for x in self._fb_host.tolist())
+            self._step_mode = 1 if heads > 0 and 2 * missed > heads else 0
+
     def stage(self, name: str, layer: int, q_pre, k_pre, v, force_miss: bool = False):
         """Launch one stage (mac_append_kv | mac_match | mac_amend | mac_complete) — for profiling/tests."""
         self._layer(layer)
+        if name == "mac_append_kv":  # a step's first stage: its match scan is chosen here
+            self._choose_match_mode()
         dt = self._check_inputs(q_pre, k_pre, v)
         _lib.call(name, self._params(layer, q_pre, k_pre, v, dt, force_miss), self._stream())
 

@@ -343,3 +343,45 @@ def test_two_pass_match_large_batch_replay(B, hq, hkv):
     # the scan's contiguous planar copy of the ring follows every write-back
     from paper_2604_00235_b200._lib import PLANAR_DIMS
     assert torch.equal(eng.ring_qp[0], eng.ring_q[0][..., :PLANAR_DIMS])
+
+
+def test_match_mode_adapts_to_misses():
+    """A miss-heavy stream on a two-pass-eligible geometry (B*Hkv >= 148, W = 512): the engine
+    reads the complete kernel's {missed, heads} feedback without synchronising and switches to
+    the one-pass scan; decisions and outputs stay those of the oracle in both modes, and a
+    pinned two-pass engine agrees with it (identical decisions, outputs to rounding)."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    B, hq, hkv, L, W, r = 37, 16, 4, 48, 512, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=500 + s,
+                                       rep_prob=0.1)) for s in range(B)]
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    pinned = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    pinned.match_mode = "two_pass"
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    oes = [orc.OracleEngine(ocfg, capacity=L + 8) for _ in range(B)]
+    q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)
+    k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)
+    v = np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)
+    modes, worst, worst_pair = [], 0.0, 0.0
+    for m in range(1, L + 1):
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a[m - 1])).to("cuda", torch.bfloat16)  # noqa: E731
+        res = eng.decode_step(0, dev(q), dev(k), dev(v))
+        modes.append(eng._step_mode)
+        gh, gp, go = res.match_hit.cpu().numpy().astype(bool), res.match_pos.cpu().numpy(), res.out.double().cpu().numpy()
+        res2 = pinned.decode_step(0, dev(q), dev(k), dev(v))
+        assert pinned._step_mode == 0
+        np.testing.assert_array_equal(res2.match_hit.cpu().numpy().astype(bool), gh)
+        np.testing.assert_array_equal(res2.match_pos.cpu().numpy(), gp)
+        go2 = res2.out.double().cpu().numpy()
+        for b in range(B):
+            st = oes[b].decode_step(0, q[m - 1, b], k[m - 1, b], v[m - 1, b], m)
+            np.testing.assert_array_equal(gh[b], st.hit)
+            np.testing.assert_array_equal(gp[b], st.p)
+            if m % 8 == 0:
+                for h in range(hq):
+                    worst = max(worst, rel_err(go[b, h], st.outputs[h]))
+                    worst_pair = max(worst_pair, rel_err(go[b, h], go2[b, h]))
+    assert 1 in modes and modes[0] == 0, modes  # switched to the one-pass scan once misses showed
+    assert worst <= TOL and worst_pair <= TOL, (worst, worst_pair)
