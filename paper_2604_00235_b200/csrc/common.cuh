@@ -199,12 +199,24 @@ __host__ __device__ __forceinline__ BandItems band_items(int m, int r, int nb) {
 // With the split band the piece is also cut into at most `ntarget` items (the amend's resident
 // warps per group, band_split's caller): as many post-wait items as warps, so no warp starts
 // a second item while the others finish (C3: 934 -> 768 items, 53.5 -> 50.0 us per step).
+// A short (hit) piece is cut into items of >= min_chunk tokens, at most ntarget of them; a long
+// piece (a group with a miss) into items of <= 256 tokens, up to max_chunks - nb — a warp
+// streams ~5 GB/s, so a few long items would serialise the step on the warps that drew them.
+// (Items of 32 tokens for C2's short pieces measured slower: 38.1 vs 35.5 us, the complete then
+// merges 17 slots.)
 __host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams& p, int m, int lo_g, int nb,
                                                           int ntarget = 0) {
   if (nb <= 0) return group_chunking(p, m, lo_g);
-  int cap = p.max_chunks - nb;
-  if (ntarget > 0 && ntarget < cap) cap = ntarget;
-  return chunking(m - p.band - grid_start(lo_g, p.kv_offset) + 1, cap, p.min_chunk);
+  const int span = m - p.band - grid_start(lo_g, p.kv_offset) + 1;
+  if (span <= 0) return chunking(span, 1, 16);
+  const int cap = p.max_chunks - nb;
+  int n = (span + p.min_chunk - 1) / p.min_chunk;
+  if (ntarget > 0 && n > ntarget) n = ntarget;
+  const int n_len = (span + 255) / 256;
+  if (n < n_len) n = n_len;
+  if (n > cap) n = cap;
+  if (n < 1) n = 1;
+  return chunking(span, n, 16);
 }
 // partial slots a group's complete merges, from its pn word (plan_group)
 __host__ __device__ __forceinline__ int group_slots(int pn_word, int m, int r) {

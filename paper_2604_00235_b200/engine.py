@@ -192,9 +192,9 @@ class BatchDecodeEngine:
         self.o_fallbacks = torch.zeros(B, Hq, **i32)
         # Match-scan choice: every 8th step the kernels store {heads that missed, heads} since
         # the last publication into this pinned buffer through its device alias; the engine
-        # reads it WITHOUT a synchronisation (so it may be ~8-16 steps old) and switch to the one-pass scan while
-        # most heads miss — the two-pass match is built for the hit path.  Both
-        # scans are exact, so a stale choice only costs time.  match_mode="two_pass" /
+        # reads it WITHOUT a synchronisation (so it may be ~8-16 steps old) and takes the
+        # one-pass scan unless misses are rare (< 1% of heads) — the two-pass match is built for
+        # the hit path.  Both scans are exact, so a stale choice only costs time.  match_mode="two_pass" /
         # "one_pass" pin it (tests, profiling); "adaptive" is the default.
         self.match_mode = "adaptive"
         self._fb_host = self._fb_alias = None
@@ -485,8 +485,12 @@ class BatchDecodeEngine:
         elif self.match_mode == "two_pass" or self._fb_host is None:
             self._step_mode = 0
         else:
+            # two-pass only while misses are rare: a single head without a near-repeat makes its
+            # verify warp walk the whole ring (~100 us), and the verify ends when its last head does
+            # (C3 geometry at 16K: 10% misses 435 us two-pass vs full attention 338 us; 30% misses
+            # 602 us two-pass, 316 us one-pass)
             missed, heads = (int(x) for x in self._fb_host.tolist())
-            self._step_mode = 1 if heads > 0 and 2 * missed > heads else 0
+            self._step_mode = 1 if heads > 0 and 100 * missed > heads else 0
 
     def stage(self, name: str, layer: int, q_pre, k_pre, v, force_miss: bool = False):
         """Launch one stage (mac_append_kv | mac_match | mac_amend | mac_complete) — for profiling/tests."""

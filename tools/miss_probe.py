@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--ctx", type=int, default=4096)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--miss-frac", type=float, default=1.0, help="fraction of heads given a fresh query")
+    ap.add_argument("--mode", default="adaptive", choices=("adaptive", "two_pass", "one_pass"))
     a = ap.parse_args()
     import bench
 
@@ -42,13 +44,17 @@ def main():
     cfg = EngineConfig(d=bench.D, d_v=bench.D, n_q_heads=32, n_kv_heads=8, window=bench.WINDOW, band=bench.BAND,
                        tau=bench.TAU, storage="bf16")
     eng = BatchDecodeEngine(cfg, a.batch, a.ctx + 64, device=dev)
+    eng.match_mode = a.mode
     inject_into_engine(eng, 0, states, n0, bulk_seed=0)
     g = torch.Generator(device=dev).manual_seed(7)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     mac, full, miss = [], [], []
+    q_rep = torch.from_numpy(np.stack([st.step_q for st in states], 1)).to(dev, torch.bfloat16)  # near-repeats
     for s in range(S):
-        q = torch.randn(a.batch, 32, bench.D, device=dev, generator=g).bfloat16()
+        fresh = torch.randn(a.batch, 32, bench.D, device=dev, generator=g).bfloat16()
+        pick = torch.rand(a.batch, 32, 1, device=dev, generator=g) < a.miss_frac
+        q = torch.where(pick, fresh, q_rep[s])
         k = torch.randn(a.batch, 8, bench.D, device=dev, generator=g).bfloat16()
         v = torch.randn(a.batch, 8, bench.D, device=dev, generator=g).bfloat16()
         for fn, acc in ((lambda: eng.decode_step(0, q, k, v), mac), (lambda: eng.full_decode(0, q, k, v), full)):
@@ -62,7 +68,8 @@ def main():
             if s >= 2:
                 acc.append(e0.elapsed_time(e1) * 1e3)
         miss.append(1.0 - float(eng.o_use.float().mean()))
-    print(json.dumps({"ctx": a.ctx, "batch": a.batch, "miss_rate": float(np.mean(miss)),
+    print(json.dumps({"ctx": a.ctx, "batch": a.batch, "mode": a.mode, "miss_frac": a.miss_frac,
+                      "miss_rate": float(np.mean(miss)),
                       "mac_us": float(np.mean(mac)), "full_us": float(np.mean(full))}))
 
 
