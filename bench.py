@@ -487,7 +487,7 @@ def run_ours(args, wl):
                          "traffic_source": "profiles/r01/ncu_traffic.json (ncu --set full, DRAM read+write per launch)"},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "StepGraph replay: pinned-host q/k/v pulled over PCIe by mac_io_copy (zero-copy kernel), step kernels, bf16 output pushed to pinned host by mac_io_copy",
+                    "path": "StepGraph replay: pinned-host q/k/v pulled over PCIe by mac_io_copy (zero-copy kernel), the step kernels, the complete kernel writing the bf16 output into the pinned host buffer (out_bf16)",
                     "output_dtype": "bf16",
                     "max_rel_diff_vs_timed_pass_fp32": e2e_vs_timed},
             # front (append + ring scan), verify, amend, complete with the two-pass match
