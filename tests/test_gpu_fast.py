@@ -5,6 +5,7 @@ reference fed storage-matched keys), on replayed traces and
 on injected long-context state where both hits and misses occur.
 """
 
+import json
 import math
 
 import numpy as np
@@ -385,3 +386,47 @@ def test_match_mode_adapts_to_misses():
                     worst_pair = max(worst_pair, rel_err(go[b, h], go2[b, h]))
     assert 1 in modes and modes[0] == 0, modes  # switched to the one-pass scan once misses showed
     assert worst <= TOL and worst_pair <= TOL, (worst, worst_pair)
+
+
+def test_bf16_storage_vs_f32_reference_distribution(capsys):
+    """SURVEY §8c gate 2b: bf16 KV/ring storage against the reference's own f32 storage on
+    identical (bf16-representable) inputs.  Storage rounding alone moves outputs by ~1e-2 at
+    the tail on this peaked workload; the gate reports mean / p99 / p99.9 / max relative error
+    and the count above the 2e-2 budget, and holds p99 within it.  Decisions may differ only
+    where the f32 reference sits at a near-tie or near the threshold."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    L, B, hq, hkv, W, r = 500, 2, 8, 2, 64, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=900 + s))
+           for s in range(B)]
+    q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)
+    k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)
+    v = np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)
+    eng = BatchDecodeEngine(EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r,
+                                         storage="bf16"), B, L + 8, min_chunk=32)
+    ocfg = orc.OracleConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="f32")
+    oes = [orc.OracleEngine(ocfg, capacity=L + 8) for _ in range(B)]
+    errs, mism, decided = [], 0, 0
+    for m in range(1, L + 1):
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a[m - 1])).to("cuda", torch.bfloat16)  # noqa: E731
+        res = eng.decode_step(0, dev(q), dev(k), dev(v))
+        gu = res.use_hit.cpu().numpy().astype(bool)
+        gp = res.match_pos.cpu().numpy()
+        go = res.out.double().cpu().numpy()
+        for b in range(B):
+            st = oes[b].decode_step(0, q[m - 1, b].astype(np.float64), k[m - 1, b].astype(np.float64),
+                                    v[m - 1, b].astype(np.float64), m)
+            for h in range(hq):
+                decided += 1
+                if gu[b, h] != st.use_hit[h] or (gu[b, h] and gp[b, h] != st.p[h]):
+                    mism += 1
+                    continue
+                errs.append(rel_err(go[b, h], st.outputs[h]))
+    e = np.array(errs)
+    stats = {"mean": float(e.mean()), "p99": float(np.quantile(e, 0.99)), "p99.9": float(np.quantile(e, 0.999)),
+             "max": float(e.max()), "over_2e-2": int((e > 2e-2).sum()), "n": int(e.size),
+             "decision_mismatch": mism, "decisions": decided}
+    with capsys.disabled():
+        print("\nbf16 storage vs f32 reference (gate 2b):", json.dumps(stats))
+    assert stats["p99"] <= 2e-2, stats
+    assert mism <= 0.01 * decided, stats
