@@ -430,3 +430,35 @@ def test_bf16_storage_vs_f32_reference_distribution(capsys):
         print("\nbf16 storage vs f32 reference (gate 2b):", json.dumps(stats))
     assert stats["p99"] <= 2e-2, stats
     assert mism <= 0.01 * decided, stats
+
+
+def test_miss_steps_equal_exact_attention():
+    """SURVEY §8c gate 4 (misses): a step that takes the miss path (here every head, through the
+    reference's refresh gate: force_miss) outputs exact attention over [1, m] — checked against
+    the device fidelity oracle (mac_attend_full) on the same bf16 cache, every head, every step,
+    with hit steps in between building the rings as usual."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    L, B, hq, hkv, W, r = 240, 2, 8, 2, 64, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=950 + s))
+           for s in range(B)]
+    q = torch.from_numpy(np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)).bfloat16()
+    k = torch.from_numpy(np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)).bfloat16()
+    v = torch.from_numpy(np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)).bfloat16()
+    eng = BatchDecodeEngine(EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r,
+                                         storage="bf16"), B, L + 8, min_chunk=32)
+    worst, checked = 0.0, 0
+    for m in range(1, L + 1):
+        miss = m % 3 == 0
+        res = eng.decode_step(0, q[m - 1].cuda(), k[m - 1].cuda(), v[m - 1].cuda(), force_miss=miss)
+        if not miss:
+            continue
+        mac = res.out.double().cpu().numpy()
+        assert not res.use_hit.cpu().numpy().any()
+        exact = eng.attend_full(0, q[m - 1].cuda()).double().cpu().numpy()
+        for b in range(B):
+            for h in range(hq):
+                checked += 1
+                worst = max(worst, rel_err(mac[b, h], exact[b, h]))
+    assert checked == (L // 3) * B * hq
+    assert worst <= 1e-4, worst
