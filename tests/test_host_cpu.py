@@ -3,6 +3,7 @@ and the C-ABI library surface (it loads and exports every declared symbol)."""
 
 import math
 import os
+import sys
 import re
 
 import numpy as np
@@ -221,3 +222,27 @@ def test_ncu_traffic_summary_matches_committed_capture():
         assert got[stage]["kernel"] == want[stage]["kernel"], stage
     # the dominant kernel moves at least its algorithmic bytes and no more than 10 % on top
     assert 87.1e6 <= want["mac_amend"]["traffic_bytes"] <= 1.1 * 87.1e6
+
+
+def test_algorithmic_step_bytes_by_hand():
+    """bench.step_bytes (the roofline's algorithmic bytes) on a case worked by hand:
+    one request, 2 q heads sharing one kv head, d = 128, W = 64, r = 16, m = 100, both heads hit
+    (p = 90 and 80) -> the group reads [min(75, 65), 100] = 36 tokens of K and V."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2604_00235_b200._lib import PLANAR_DIMS as P
+
+    use = np.array([[1, 1]])
+    pos = np.array([[90, 80]])
+    b = bench.step_bytes(use, pos, np.array([100]), hq=2, hkv=1, d=128, window=64, band=16)
+    assert b["amend"] == 36 * 2 * 128 * 2
+    assert b["match"] == 2 * (64 * P * 2 + 64 * 4 + 1 * 16 + 128 * 2)
+    assert b["verify"] == 2 * (1 * 16 + 2 * (128 - P) * 2 + 128 * 2)
+    assert b["complete"] == 2 * (128 * 4 + 4) + 2 * (128 * 2 + P * 2 + 128 * 4 + 4) + 2 * 128 * 4
+    assert b["append"] == 1 * 2 * 128 * 2
+    assert b["total"] == sum(b[k] for k in ("match", "verify", "amend", "complete", "append"))
+    # a miss reads the group's whole context
+    b2 = bench.step_bytes(np.array([[0, 1]]), pos, np.array([100]), hq=2, hkv=1, d=128, window=64, band=16)
+    assert b2["amend"] == 100 * 2 * 128 * 2
