@@ -177,7 +177,9 @@ int piece_target(const MacDecodeParams& p) {
 }
 
 cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, bool full_spans) {
-  const int vi = amend_variant(full_spans);
+  // the KV-sharded path (n_shards > 0: one very long request, the miss path) is long-span work
+  // too: the full-span variant streams it faster (C4, one 512K request: 0.457 -> 0.421 ms)
+  const int vi = amend_variant(full_spans || p.n_shards > 0);
   const AmendVariant& v = kAmendVariants[vi];
   cudaError_t err = cudaSuccess;
   const int gfull = amend_grid_full(vi, &err);
