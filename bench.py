@@ -240,13 +240,105 @@ def cpu_model():
     return "unknown"
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "attnreuse"))
+
+
+def _ref_worker(args):
+    """One request through the UNMODIFIED reference package (baseline/_ref/attnreuse,
+    DecodeEngine.decode_step, engine.py:410-539) on one host core.  The decode state at n0 is
+    injected into the reference's own containers (KvStore head buffers, QueryRing,
+    SummaryRing) before timing — the reference has no prefill, and replaying 128K steps per
+    request is out of reach on a CPU — then every timed step is a stock decode_step call.
+    Storage: the reference's f32 store (it has no bf16 mode) holding the same bf16-rounded
+    keys/values the GPU reads, so both sides see identical values."""
+    seed, n0, steps, warm = args
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import attnreuse as ar
+    from attnreuse import engine as ar_engine
+    from attnreuse import kvstore as ar_kv
+    from paper_2604_00235_b200.synth import request_state
+
+    wl = _CPU_WL
+    hq, hkv = wl["hq"], wl["hkv"]
+    st = request_state(seed, n0=n0, steps=warm + steps, hq=hq, hkv=hkv, d=D, dv=D, window=WINDOW, band=BAND)
+    cfg = ar.EngineConfig(d=D, d_v=D, n_layers=1, n_q_heads=hq, n_kv_heads=hkv, window=WINDOW, band=BAND,
+                          tau=TAU, storage="f32")
+    eng = ar.DecodeEngine(cfg)
+    T = st.tail_k.shape[1]
+    cap = n0 + warm + steps + 64
+    for j in range(hkv):
+        buf = ar_kv._HeadBuffer(D, D)
+        buf.keys = np.zeros((cap, D))   # lazily mapped: only the tail pages are touched
+        buf.values = np.zeros((cap, D))
+        buf.keys[n0 - T:n0] = st.tail_k[j]
+        buf.values[n0 - T:n0] = st.tail_v[j]
+        buf.n = n0
+        eng.store._heads[(0, j)] = buf
+    pos = np.arange(n0 - WINDOW + 1, n0 + 1)
+    slots = (pos - 1) % WINDOW
+    for h in range(hq):
+        qr, sr = eng.rings(0, h)
+        qr._q[slots] = st.ring_q[h]
+        qr._sqnorm[slots] = np.einsum("wd,wd->w", st.ring_q[h].astype(np.float64), st.ring_q[h].astype(np.float64))
+        qr._pos[slots] = pos
+        qr._count = n0
+        for i, (p, sl) in enumerate(zip(pos, slots)):
+            sr._items[sl] = ar_engine.AttentionSummary(acc=st.ring_acc[h, i].astype(np.float64),
+                                                       lse=float(st.ring_lse[h, i]), count=max(0, int(p) - BAND))
+        sr._pos[slots] = pos
+        sr._count = n0
+    times, outs, hits = [], [], 0
+    for s in range(warm + steps):
+        t0 = time.perf_counter()
+        r = eng.decode_step(0, st.step_q[s], st.step_k[s], st.step_v[s], n0 + s + 1)
+        dt = time.perf_counter() - t0
+        if s >= warm:
+            times.append(dt)
+        outs.append(r.outputs)
+        hits += sum(1 for c in r.cached_summaries if c is not None)
+    return times, np.stack(outs), hits
+
+
+def ref_reference(wl, n0, steps, warm, procs, seeds):
+    global _CPU_WL
+    _CPU_WL = wl
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_worker, [(sd, n0, steps, warm) for sd in seeds])
+    wall = time.perf_counter() - t0
+    per_step = [t for r in res for t in r[0]]
+    return {
+        "per_step_s_mean": float(np.mean(per_step)),
+        "tokens_per_s": len(seeds) / float(np.mean([sum(r[0]) / len(r[0]) for r in res])),
+        "hits": sum(r[2] for r in res), "wall_s": wall,
+    }
+
+
 def run_reference_arm(args, wl):
-    """--impl reference: the reference algorithm on host cores (numpy restatement, bf16 storage)."""
+    """--impl reference: the reference's own CPU implementation of the path (the unmodified
+    `attnreuse` package installed in baseline/_ref) on the host cores, one request per process,
+    on this workload; the numpy restatement in oracle/ stands in only when baseline/_ref is
+    absent (kind "port")."""
     cores = os.cpu_count() or 1
     procs = max(1, min(cores, args.cpu_procs or cores, wl["batch"]))
     n0 = wl["ctx"] - args.warmup - args.steps - 1
     seeds = list(range(procs))
-    r = cpu_reference(wl, n0, args.steps, args.warmup, procs, seeds)
+    if reference_available():
+        r = ref_reference(wl, n0, args.steps, args.warmup, procs, seeds)
+        kind, what = "reference", "the unmodified reference package (baseline/_ref/attnreuse, DecodeEngine.decode_step, f32 store)"
+        dtype = "f64 math / f32 store of bf16-rounded values"
+    else:
+        r = cpu_reference(wl, n0, args.steps, args.warmup, procs, seeds)
+        kind, what = "port", "oracle/ numpy restatement (baseline/_ref absent)"
+        dtype = "f64 math / bf16-rounded storage"
     val = r["tokens_per_s"]
     line = {
         "impl": "reference",
@@ -260,12 +352,14 @@ def run_reference_arm(args, wl):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64 math / bf16-rounded storage",
+        "dtype": dtype,
         "data": "synthetic injected state (paper_2604_00235_b200/synth.py)",
         "config": {"workload": wl["desc"] + " — CPU sample", "requests_sampled": procs, "context": wl["ctx"],
                    "window": WINDOW, "band": BAND, "tau": TAU},
-        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} requests x {args.steps} steps (1 process each), model {cpu_model()}"},
+        "hit_rate": r["hits"] / max(1, procs * (args.steps + args.warmup) * wl["hq"]),
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": procs, "kind": kind,
+                         "sample": f"{procs} requests x {args.steps} timed steps (1 process each) of {what}, "
+                                   f"model {cpu_model()}"},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -294,6 +388,15 @@ def run_ours(args, wl):
     n0 = wl["ctx"] - S - 1
     seeds = [rank * B + b for b in range(B)]
     states = make_states(seeds, n0=n0, steps=S, hq=hq, hkv=hkv, d=D, dv=D, window=WINDOW, band=BAND)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sub = None
+    if args.workload == "c3" and world == 1 and not args.no_sub:
+        # the 32K point of the headline metric (C2), measured in the same run as a sub-record
+        wl2 = WORKLOADS["c2"]
+        S2 = args.warmup + min(args.steps, 20)
+        n2 = wl2["ctx"] - S2 - 1
+        sub = (wl2, n2, S2, make_states([10_000 + b for b in range(wl2["batch"])], n0=n2, steps=S2, hq=wl2["hq"],
+                                        hkv=wl2["hkv"], d=D, dv=D, window=WINDOW, band=BAND))
 
     import torch
     import torch.distributed as dist
@@ -301,12 +404,16 @@ def run_ours(args, wl):
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
     from paper_2604_00235_b200.synth import inject_into_engine
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nccl_ranks = 1
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        nccl_ranks = dist.get_world_size()
+        if rank == 0:
+            print(f"bench: NCCL process group of {nccl_ranks} ranks (request-sharded, no data-path collective)",
+                  file=sys.stderr, flush=True)
 
     W_, K = args.warmup, args.steps
     cfg = EngineConfig(d=D, d_v=D, n_q_heads=hq, n_kv_heads=hkv, window=WINDOW, band=BAND, tau=TAU, storage="bf16",
@@ -374,7 +481,9 @@ def run_ours(args, wl):
     use = use_log.cpu().numpy()
     pos = pos_log.cpu().numpy()
     mm = m_log.cpu().numpy()
-    two_pass = os.environ.get("MAC_FRONT_VARIANT", "0") in ("0", "4", "5", "6", "7")
+    from paper_2604_00235_b200 import _lib as mac_lib
+
+    two_pass = bool(eng.match_path() & mac_lib.PATH_TWO_PASS)  # the scan the timed steps ran
     byts = [step_bytes(use[s], pos[s], mm[s], hq, hkv, D, WINDOW, BAND, two_pass=two_pass) for s in range(W_, S)]
     hit_rate = float(use[W_:].mean())
 
@@ -437,6 +546,11 @@ def run_ours(args, wl):
     dom = max(("mac_match_scan", "mac_amend"), key=lambda n: kern[n]["bytes"])
     step_gbs = mean_b["total"] / (ms_per_step * 1e-3) / 1e9
 
+    sub_rec = None
+    if sub is not None:
+        del sg
+        sub_rec = measure_sub(args, dev, *sub)
+
     result = None
     if rank == 0:
         cpu = None
@@ -471,7 +585,8 @@ def run_ours(args, wl):
             "config": {"workload": wl["desc"], "batch_per_gpu": B, "global_batch": B * world, "context": wl["ctx"],
                        "hq": hq, "hkv": hkv, "d": D, "window": WINDOW, "band": BAND, "tau": TAU,
                        "page_size": args.page_size, "variant": "hit path (rep_prob=1, noise 0.05, gap<=512)",
-                       "l2": f"flushed (256 MiB {FLUSH_MODE}) between steps", "parallelism": f"request-sharded x{world}"},
+                       "l2": f"flushed (256 MiB {FLUSH_MODE}) between steps", "parallelism": f"request-sharded x{world}",
+                       "nccl_ranks": nccl_ranks},
             "per_token_latency_us": ms_per_step * 1e3,
             "hit_rate": hit_rate,
             "kv_gbs": step_gbs,
@@ -496,6 +611,8 @@ def run_ours(args, wl):
             "gpu_launches": (4 if two_pass and B * hq >= 148 else 3) * K,
             "clocks": clk.summary(),
         }
+        if sub_rec is not None:
+            result["c2"] = sub_rec
         if cpu is not None:
             result["cpu_baseline"] = {"value": cpu["tokens_per_s"], "unit": "tokens/s", "cores": procs, "kind": "port",
                                       "sample": f"{procs} requests x {args.cpu_steps} steps of this workload "
@@ -506,6 +623,66 @@ def run_ours(args, wl):
     if world > 1:
         dist.destroy_process_group()
     return result
+
+
+def measure_sub(args, dev, wl, n0, S, states):
+    """A second workload's MAC step and full-attention baseline on this GPU (the C2 point of the
+    headline metric: B = 8, 32K): same protocol as the main line (L2 flushed before every step,
+    CUDA events on the launching stream), fewer steps."""
+    import torch
+
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
+    from paper_2604_00235_b200.synth import inject_into_engine
+
+    B, hq, hkv = wl["batch"], wl["hq"], wl["hkv"]
+    cfg = EngineConfig(d=D, d_v=D, n_q_heads=hq, n_kv_heads=hkv, window=WINDOW, band=BAND, tau=TAU, storage="bf16",
+                       page_size=args.page_size)
+    eng = BatchDecodeEngine(cfg, B, wl["ctx"] + args.full_steps + 64, device=dev, min_chunk=args.min_chunk)
+    inject_into_engine(eng, 0, states, n0, bulk_seed=77)
+    bf = torch.bfloat16
+    q_all = torch.from_numpy(np.stack([s.step_q for s in states], 1)).to(dev, bf)
+    k_all = torch.from_numpy(np.stack([s.step_k for s in states], 1)).to(dev, bf)
+    v_all = torch.from_numpy(np.stack([s.step_v for s in states], 1)).to(dev, bf)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+    use_log, pos_log, m_log = [], [], []
+    torch.cuda.synchronize(dev)
+    for s in range(S):
+        l2_flush(flush)
+        torch.cuda._sleep(200_000)
+        ev[s][0].record(stream)
+        eng.decode_step(0, q_all[s], k_all[s], v_all[s])
+        ev[s][1].record(stream)
+        use_log.append(eng.o_use.clone())
+        pos_log.append(eng.o_pos.clone())
+        m_log.append(eng.seq_lens[0].clone())
+    torch.cuda.synchronize(dev)
+    W_ = args.warmup
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev[W_:]]))
+    byts = [step_bytes(use_log[s].cpu().numpy(), pos_log[s].cpu().numpy(), m_log[s].cpu().numpy(), hq, hkv, D,
+                       WINDOW, BAND)["total"] for s in range(W_, S)]
+    F = max(3, min(S - W_, args.full_steps))
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(F + 2)]
+    fm = []
+    for s in range(F + 2):
+        l2_flush(flush)
+        fev[s][0].record(stream)
+        eng.full_decode(0, q_all[s % S], k_all[s % S], v_all[s % S])
+        fev[s][1].record(stream)
+        fm.append(eng.seq_lens[0].clone())
+    torch.cuda.synchronize(dev)
+    full_ms = float(np.mean([a.elapsed_time(b) for a, b in fev[2:]]))
+    peak, peak_kind = measured_peak_gbs()
+    gbs = float(np.mean(byts)) / (ms * 1e-3) / 1e9
+    rec = {"workload": wl["desc"], "steps": S - W_, "ms_per_step": ms, "per_token_latency_us": ms * 1e3,
+           "value": B / (ms * 1e-3), "unit": "tokens/s",
+           "hit_rate": float(torch.stack(use_log[W_:]).float().mean()),
+           "bytes_per_step": float(np.mean(byts)), "kv_gbs": gbs, "frac_of_peak": gbs / peak, "peak_kind": peak_kind,
+           "full_attention_ms": full_ms, "speedup_vs_full_attention": full_ms / ms}
+    del eng
+    torch.cuda.empty_cache()
+    return rec
 
 
 # ----------------------------------------------------------------------------
@@ -631,7 +808,22 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--flush", default="write+read", choices=("write+read", "write"),
                     help="L2 flush between timed steps (see l2_flush)")
+    ap.add_argument("--no-sub", action="store_true", help="skip the C2 sub-record of the default c3 line")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch this command under torchrun (the driver's own launch
+        # sets WORLD_SIZE and lands below)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world_env != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world_env}; measuring {world_env} ranks", file=sys.stderr)
     global FLUSH_MODE
     FLUSH_MODE = args.flush
     wl = WORKLOADS[args.workload]

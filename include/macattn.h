@@ -201,6 +201,9 @@ size_t mac_params_size(void);
 const char* mac_error_string(int code);
 /* bytes of scratch the decode entry points need for this geometry */
 size_t mac_workspace_bytes(const MacDecodeParams* p);
+/* byte offset in the workspace of a sticky uint32 flag that an append sets when a token has no
+ * page in its request's page_table row (the token is then not stored); 0 while every append fit */
+size_t mac_overflow_flag_offset(const MacDecodeParams* p);
 /* which kernel family mac_amend would launch: 0 generic CUDA-core, 1 bf16 tensor-core (mma) */
 int mac_amend_variant(const MacDecodeParams* p);
 

@@ -26,6 +26,7 @@ EXPORTS = (
     "mac_params_size",
     "mac_error_string",
     "mac_workspace_bytes",
+    "mac_overflow_flag_offset",
     "mac_amend_variant",
     "mac_append_kv",
     "mac_match",
@@ -164,6 +165,8 @@ def load() -> C.CDLL:
     lib.mac_error_string.argtypes = [C.c_int]
     lib.mac_workspace_bytes.restype = C.c_size_t
     lib.mac_workspace_bytes.argtypes = [C.POINTER(MacDecodeParams)]
+    lib.mac_overflow_flag_offset.restype = C.c_size_t
+    lib.mac_overflow_flag_offset.argtypes = [C.POINTER(MacDecodeParams)]
     lib.mac_amend_variant.restype = C.c_int
     lib.mac_amend_variant.argtypes = [C.POINTER(MacDecodeParams)]
     for name in ("mac_append_kv", "mac_match", "mac_match_scan", "mac_match_verify", "mac_amend", "mac_complete", "mac_decode_step", "mac_full_decode",

@@ -25,12 +25,21 @@ INCLUDE = os.path.join(ROOT, "include")
 # %globaltimer at entry / after the grid-dependency wait / exit into the workspace
 # (tools/timeline.py reads it); the product library is never built with it.
 TIMELINE = os.environ.get("MAC_TIMELINE") == "1"
-OBJ = os.path.join(ROOT, "build", "obj_tl" if TIMELINE else "obj")
-LIB = os.path.join(PKG, "lib", "libmacattn_tl.so" if TIMELINE else "libmacattn.so")
+DEV = os.environ.get("MAC_DEV_KNOBS") == "1"
+OBJ = os.path.join(ROOT, "build", "obj_tl" if TIMELINE else ("obj_dev" if DEV else "obj"))
+LIB = os.path.join(PKG, "lib", "libmacattn_tl.so" if TIMELINE else ("libmacattn_dev.so" if DEV else "libmacattn.so"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--use_fast_math", "-Xcompiler", "-fPIC,-O3",
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3",
               "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC] + (["-DMAC_TIMELINE"] if TIMELINE else [])
+# MAC_DEV_KNOBS=1 compiles the development variant tables and their environment selectors
+# (MAC_FRONT_VARIANT, ...) into the library; the product library has neither.
+if os.environ.get("MAC_DEV_KNOBS") == "1":
+    NVCC_FLAGS.append("-DMAC_DEV_KNOBS")
+# --use_fast_math only for the bf16 d = 128 fast-path kernels (their fp32 softmax and distance
+# math is written for it and parity-gated at 1e-4); the generic f32 / f64 kernels compile with
+# IEEE division, square root and denormals
+FAST_MATH = {"amend_mma.cu", "match_fast.cu", "tma_amend.cu"}
 
 
 def nvcc() -> str:
@@ -50,7 +59,8 @@ def _compile(src: str, force: bool, verbose: bool) -> str:
     if not force and os.path.exists(obj):
         if os.path.getmtime(obj) >= max(os.path.getmtime(src), _headers_mtime()):
             return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    fm = ["--use_fast_math"] if os.path.basename(src) in FAST_MATH else []
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *fm, "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, 
   // the work counters are returned to zero by the complete kernel (after this grid)
 }
 
-// Variants (stages, min warps per SM); MAC_AMEND_VARIANT selects one (development knob).
+// Variants (stages, min warps per SM); development builds (-DMAC_DEV_KNOBS) select one with
+// MAC_AMEND_VARIANT.
 struct AmendVariant {
   void (*fn)(MacDecodeParams, int);
   int smem;
@@ -123,13 +124,16 @@ constexpr int kAmendN = (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0])
 // short spans prefer 4 stages at 6 warps per SM (81.0 vs 84.5 us).  MAC_AMEND_VARIANT
 // overrides both.
 static int amend_variant(bool full_spans) {
+#ifdef MAC_DEV_KNOBS
   static int forced = -2;
   if (forced == -2) {
     const char* env = getenv("MAC_AMEND_VARIANT");
     forced = env ? atoi(env) : -1;
     if (forced >= kAmendN) forced = -1;
   }
-  return forced >= 0 ? forced : (full_spans ? 3 : 0);
+  if (forced >= 0) return forced;
+#endif
+  return full_spans ? 3 : 0;
 }
 
 // resident warps of a variant's persistent grid (sets the smem attribute on first use)
@@ -152,14 +156,18 @@ static int amend_grid_full(int vi, cudaError_t* err) {
 // not split it: the hit step of the fast path only — the two-pass front (whose verify kernel
 // the band overlaps, and which guarantees the append finished before this grid launches),
 // one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
-// (1..4).  MAC_BAND_SPLIT=0 turns it off, =n forces n items (development knobs).  The verify
+// (1..4).  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
 // kernel's plan and this launch call it with the same parameters, so they always agree.
 int band_split(const MacDecodeParams& p) {
+#ifdef MAC_DEV_KNOBS
   static int forced = -2;
   if (forced == -2) {
     const char* env = getenv("MAC_BAND_SPLIT");
     forced = env ? atoi(env) : -1;
   }
+#else
+  const int forced = -1;
+#endif
   if (forced == 0 || !amend_mma_supported(p) || !front_two_pass(p) || p.kv_offset != 0 || p.kv_limit != 0 ||
       p.band <= 0)
     return 0;

@@ -210,7 +210,7 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
     const int j = blk * 32 + lane;
     if (j >= nsub) return 0;
     const int local = t0 + (j << 4) - p.kv_offset;
-    const int page = p.page_table[(int64_t)b * p.pages_per_seq + (local - 1) / ps];
+    const int page = p.page_table[(int64_t)b * p.pages_per_seq + min((local - 1) / ps, p.pages_per_seq - 1)];
     return ((long long)page * Hkv + kvh) * ps + ((local - 1) % ps);
   };
   long long rows_cur = rows_of(0), rows_nxt = nsub > 32 ? rows_of(1) : 0;

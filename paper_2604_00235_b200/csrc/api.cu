@@ -122,6 +122,7 @@ const char* mac_error_string(int code) {
 }
 
 size_t mac_workspace_bytes(const MacDecodeParams* p) { return p ? workspace_layout(*p).total : 0; }
+size_t mac_overflow_flag_offset(const MacDecodeParams* p) { return p ? workspace_layout(*p).ctr_off + 8 : 0; }
 
 #ifdef MAC_TIMELINE
 // development builds only (not in macattn.h): byte offset of the timeline stamps in the workspace

@@ -25,7 +25,11 @@ __global__ void __launch_bounds__(256) append_rope_kernel(MacDecodeParams p, int
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
   const int t_local = m - p.kv_offset;        // position inside this shard's cache
   if (threadIdx.x == 0) mpos[b] = m;
-  const bool store_kv = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
+  bool store_kv = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
+  if (store_kv && !kv_fits(p.pages_per_seq, t_local, p.page_size)) {
+    store_kv = false;
+    if (threadIdx.x == 0) atomicOr(ws_ptr<unsigned>(p, workspace_layout(p).ctr_off) + 2, 1u);
+  }
   int64_t row = 0;
   if (store_kv) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
   kv_t* kc = static_cast<kv_t*>(p.k_cache);

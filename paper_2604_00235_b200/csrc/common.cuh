@@ -228,8 +228,17 @@ __host__ __device__ __forceinline__ int group_slots(int pn_word, int m, int r) {
 __device__ __forceinline__ int64_t kv_row(const int32_t* __restrict__ page_table, int pages_per_seq,
                                           int b, int t, int page_size, int n_kv, int kvh) {
   int idx = t - 1;
-  int page = page_table[(int64_t)b * pages_per_seq + idx / page_size];
+  int pi = idx / page_size;
+  pi = pi < pages_per_seq ? pi : pages_per_seq - 1;  // never past the request's table row (see kv_fits)
+  int page = page_table[(int64_t)b * pages_per_seq + pi];
   return ((int64_t)page * n_kv + kvh) * page_size + (idx % page_size);
+}
+
+// whether token t (1-based, shard-local) has a page in the request's table row.  The appends
+// store only when it does and otherwise raise the overflow flag (workspace ctr[2], read by
+// BatchDecodeEngine.check_overflow); the engine grows the pool before a step would need it.
+__device__ __forceinline__ bool kv_fits(int pages_per_seq, int t, int page_size) {
+  return t >= 1 && (t - 1) / page_size < pages_per_seq;
 }
 
 // workspace layout (bytes, 256-aligned sections)
@@ -253,7 +262,8 @@ struct Workspace {
   size_t ctr_off;    // [16] u32     0 work-list length, 1 amend work counter (both reset by complete),
                      //              4 heads missed and 6 steps completed since the feedback was last published
                      //              (complete adds; every 8th step's append warps publish and reset)
-                     //              (2-15 spare)
+                     //              2 KV overflow flag (an append found no page for its token; sticky)
+                     //              (3, 5, 7-15 spare)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  piece splits planned for the group | band items requested << 16
   size_t mpos_off;   // [B] i32      position m of this step

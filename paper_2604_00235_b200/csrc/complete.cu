@@ -209,11 +209,14 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
       if (h == 0) p.seq_lens[b] = m;
     }
   }
-  // heads that missed this step, counted fire-and-forget (RED); the next step's append warps
-  // publish the count to `feedback` (front.cuh)
-  if (p.feedback && live && lane == 0 && !(p.force_miss ? 0 : __ldcg(p.use_hit + bh)))
-    atomicAdd(ws_ptr<unsigned>(p, wsl.ctr_off) + 4, 1u);
-  if (p.feedback && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ws_ptr<unsigned>(p, wsl.ctr_off) + 6, 1u);
+  // heads whose raw match missed this step (the case that makes the two-pass verify walk the
+  // ring; gate-forced misses do not), counted fire-and-forget (RED); a forced-miss step (prefill,
+  // force_miss) is not counted at all.  A later step's append warps publish the count to
+  // `feedback` (front.cuh).
+  if (p.feedback && !p.force_miss) {
+    if (live && lane == 0 && !__ldcg(p.match_hit + bh)) atomicAdd(ws_ptr<unsigned>(p, wsl.ctr_off) + 4, 1u);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ws_ptr<unsigned>(p, wsl.ctr_off) + 6, 1u);
+  }
 #ifdef MAC_TIMELINE
   __syncthreads();
 #endif

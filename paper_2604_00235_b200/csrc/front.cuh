@@ -20,9 +20,11 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
   const Workspace w = workspace_layout(p);
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
   if (lane == 0) ws_ptr<int>(p, w.mpos_off)[b] = m;  // every group's warp (same value)
-  // every 8th step: the misses counted since the last publication (complete.cu) -> host.  Not
+  // every 8th token: the misses counted since the last publication (complete.cu) -> host.  Not
   // every step: a kernel that stores to host memory pays for the flush when it ends (~1 us).
-  if (idx == 0 && lane == 0 && p.feedback && (m & 7) == 0) {
+  // With several layers per token every layer's complete counts into the same counters and only
+  // the first layer stepped at that token publishes (>= 8 steps counted since the last one).
+  if (idx == 0 && lane == 0 && p.feedback && (m & 7) == 0 && ws_ptr<unsigned>(p, w.ctr_off)[6] >= 8u) {
     unsigned* ctr = ws_ptr<unsigned>(p, w.ctr_off);
     p.feedback[0] = (int)ctr[4];
     p.feedback[1] = (int)ctr[6] * p.batch * p.n_q_heads;
@@ -30,7 +32,11 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
     ctr[6] = 0u;
   }
   const int t_local = m - p.kv_offset;
-  const bool store = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
+  bool store = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
+  if (store && !kv_fits(p.pages_per_seq, t_local, p.page_size)) {
+    store = false;
+    if (lane == 0) atomicOr(ws_ptr<unsigned>(p, w.ctr_off) + 2, 1u);
+  }
   int64_t row = 0;
   if (store) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
   __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);

@@ -493,13 +493,14 @@ bool front_fast_supported(const MacDecodeParams& p) {
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128;
 }
 
-// MAC_FRONT_VARIANT (development knob): two-pass match, (ring rows per CTA, min CTAs per SM,
-// first-pass dims) = 0: (512, 4, 16) default, reading ring_qp when given; 6: (512, 4, 32); 4: (256, 4, 64) on
-// ring_q; 5: (256, 4, 32); one-pass stream 1-3: (128,5), (64,8), (256,3).  C3 step (us):
-// 59.8 (0), 67.8 (4); the (256,6) and (512,3) shapes scanned 3.5 and 0.8 us slower than (0).
-// Measured alternatives that lost on C3 (persistent tensor-core, persistent CUDA-core, f32x2
-// "lean", DSMEM-cluster argmin, one fused step kernel) are on branch exp/fused-step; numbers
-// in DESIGN.md §4.
+// Front variants: two-pass match (ring rows per CTA, min CTAs per SM, first-pass dims) =
+// (512, 4, 16) reading ring_qp when given (the product), and the one-pass stream (128, 5).
+// Development builds (-DMAC_DEV_KNOBS) add the measured alternatives, selected with
+// MAC_FRONT_VARIANT: 2-3 one-pass (64, 8), (256, 3); 4-7 two-pass (256, 4, 64), (256, 4, 32),
+// (512, 4, 32), (1024, 4, 16).  C3 step (us): 59.8 (0), 67.8 (4); the (256,6) and (512,3)
+// shapes scanned 3.5 and 0.8 us slower than (0).  Round-1 alternatives that lost on C3
+// (persistent tensor-core and CUDA-core scans, a DSMEM-cluster argmin, one fused step kernel)
+// were measured and not kept; their numbers are in profiles/r01/SUMMARY.md.
 struct FrontVariant {
   void (*fn)(MacDecodeParams, int, int, int, int, int);
   int rows;
@@ -510,17 +511,20 @@ struct FrontVariant {
 static const FrontVariant kFrontVariants[] = {
     {front_half_kernel<512, 4, 16>, 512, true, 16, front_half_kernel<512, 4, 16, true>},
     {front_bf16_d128_kernel<128, 5>, 128, false, 0, nullptr},
+#ifdef MAC_DEV_KNOBS
     {front_bf16_d128_kernel<64, 8>, 64, false, 0, nullptr},
     {front_bf16_d128_kernel<256, 3>, 256, false, 0, nullptr},
     {front_half_kernel<256, 4, 64>, 256, true, 64, nullptr},
     {front_half_kernel<256, 4, 32>, 256, true, 32, nullptr},
     {front_half_kernel<512, 4, 32>, 512, true, 32, nullptr},
     {front_half_kernel<1024, 4, 16>, 1024, true, 16, front_half_kernel<1024, 4, 16, true>},
+#endif
 };
 
 // append CTAs first (8 warps, one (request, kv head) each), then the match CTAs
 // passes: bit 0 = the scan (append, rows), bit 1 = the verify kernel (two-pass mode only)
 static int front_variant() {
+#ifdef MAC_DEV_KNOBS
   static int vi = -1;
   if (vi < 0) {
     const char* env = getenv("MAC_FRONT_VARIANT");
@@ -528,8 +532,11 @@ static int front_variant() {
     if (vi < 0 || vi >= (int)(sizeof(kFrontVariants) / sizeof(kFrontVariants[0]))) vi = 0;
   }
   return vi;
+#else
+  return 0;
+#endif
 }
-static bool verify_per_group(const MacDecodeParams& p) {
+bool verify_per_group(const MacDecodeParams& p) {
   return p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
 }
 // whether a match launch of the fast front runs the two-pass scan + verify kernels: enough heads

@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(256) prefill_kv_kernel(MacDecodeParams p, int 
   const int pos = p.seq_lens[b] + 1 + t;
   const int local = pos - p.kv_offset;
   if (local < 1 || (p.kv_limit > 0 && local > p.kv_limit)) return;
+  if (!kv_fits(p.pages_per_seq, local, p.page_size)) {
+    if (lane == 0) atomicOr(ws_ptr<unsigned>(p, workspace_layout(p).ctr_off) + 2, 1u);
+    return;
+  }
   const int64_t row = kv_row(p.page_table, p.pages_per_seq, b, local, p.page_size, Hkv, kvh);
   const int64_t src = (((int64_t)b * n_tokens + t) * Hkv + kvh);
   kv_t* kc = static_cast<kv_t*>(p.k_cache);

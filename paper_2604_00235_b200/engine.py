@@ -165,6 +165,11 @@ class BatchDecodeEngine:
         dev = self.device
         self.freqs = torch.from_numpy(rope_freqs(cfg.d, cfg.rope_base)).to(dev)
         self.capacity = 0
+        # host mirror of the tokens stored per layer (max over requests): the engine grows the
+        # paged pool before a step would need a page it does not have (the reference KvStore
+        # grows on demand, kvstore.py:105-119); the appends also refuse such tokens on the device
+        # and raise a sticky flag (check_overflow)
+        self._len = [0] * cfg.n_layers
         self.k_cache: list[torch.Tensor] = []
         self.v_cache: list[torch.Tensor] = []
         self.page_table = None
@@ -252,18 +257,39 @@ class BatchDecodeEngine:
         if tokens > self.capacity:
             self._alloc_kv(max(tokens, 2 * self.capacity))
 
+    def _local_tokens(self, layer: int, n_new: int) -> int:
+        """Shard-local tokens this layer holds after n_new more appends."""
+        need = self._len[layer] + n_new - self.kv_offset
+        return min(need, self.kv_limit) if self.kv_limit > 0 else need
+
+    def _ensure_room(self, layer: int, n_new: int = 1, *, grow: bool = True):
+        need = self._local_tokens(layer, n_new)
+        if need > self.capacity:
+            if not grow:
+                raise ValueError(f"layer {layer}: position {self._len[layer] + n_new} exceeds the KV capacity "
+                                 f"{self.capacity}; reserve() before capturing a StepGraph")
+            self.reserve(need)
+
+    def check_overflow(self) -> bool:
+        """True when any append since construction found no page for its token (synchronises)."""
+        off = int(_lib.load().mac_overflow_flag_offset(self._params(0, self.o_out, self.o_out, self.o_out,
+                                                                    _lib.DT_F32)))
+        return int(self.workspace[off:off + 4].view(torch.int32).item()) != 0
+
     # ------------------------------------------------------------------ launch
     def _params(self, layer: int, q, k, v, in_dt: int, force_miss: bool = False) -> _lib.MacDecodeParams:
         key = (layer, q.data_ptr(), k.data_ptr(), v.data_ptr(), in_dt, force_miss)
         cache = self.__dict__.setdefault("_pcache", {})
-        hit = cache.get(key)
-        if hit is not None:
-            return hit
-        P = self._build_params(layer, q, k, v, in_dt, force_miss)
-        if hasattr(self, "workspace"):
-            if len(cache) > 256:
-                cache.clear()
-            cache[key] = P
+        P = cache.get(key)
+        if P is None:
+            P = self._build_params(layer, q, k, v, in_dt, force_miss)
+            if hasattr(self, "workspace"):
+                if len(cache) > 256:
+                    cache.clear()
+                cache[key] = P
+        # per-call fields: the step's scan choice and no output narrowing unless the caller sets it
+        P.match_mode = self._step_mode
+        P.out_bf16 = None
         return P
 
     def _build_params(self, layer: int, q, k, v, in_dt: int, force_miss: bool) -> _lib.MacDecodeParams:
@@ -350,9 +376,12 @@ class BatchDecodeEngine:
         refresh gate does (engine.py:456-459)."""
         self._layer(layer)
         dt = self._check_inputs(q_pre, k_pre, v)
+        self._ensure_room(layer)
         self._choose_match_mode()
         P = self._params(layer, q_pre, k_pre, v, dt, force_miss)
+        self.last_params = P  # what the library was given (tests: mac_match_path(last_params))
         _lib.call("mac_decode_step", P, self._stream())
+        self._len[layer] += 1
         if self.track_stats and not getattr(self, "_in_prefill", False):
             self._accumulate_stats(layer, P)
         return self.result()
@@ -360,9 +389,9 @@ class BatchDecodeEngine:
     def _decode_step_ptrs(self, layer: int, q_ptr: int, k_ptr: int, v_ptr: int, in_dt: int, out_bf16: int = 0):
         """decode_step on raw device pointers, optionally also writing the output narrowed to
         bf16 at `out_bf16` (a pinned host buffer's device alias: StepGraph's zero-copy output)."""
-        self._choose_match_mode()
         P = self._params(layer, _Ptr(q_ptr), _Ptr(k_ptr), _Ptr(v_ptr), in_dt, False)
         P.out_bf16 = out_bf16 or None
+        self.last_params = P
         _lib.call("mac_decode_step", P, self._stream())
         if self.track_stats and not getattr(self, "_in_prefill", False):
             self._accumulate_stats(layer, P)
@@ -459,7 +488,8 @@ class BatchDecodeEngine:
         if n == 0:
             return None
         stored = int(self.seq_lens[layer].max().item()) if self.capacity else 0
-        self.reserve(stored + n + 1)
+        self._len[layer] = max(self._len[layer], stored)
+        self._ensure_room(layer, n + 1)
         n_bulk = n - min(n, cfg.window)
         if n_bulk:
             kb, vb = k_pre[:, :n_bulk].contiguous(), v[:, :n_bulk].contiguous()
@@ -468,6 +498,7 @@ class BatchDecodeEngine:
             P = self._build_params(layer, q0, kb, vb, dt, False)
             code = _lib.load().mac_prefill_kv(P, n_bulk, self._stream())
             _lib.check(code, "mac_prefill_kv")
+            self._len[layer] += n_bulk
         res = None
         self._in_prefill = True  # prompt tokens are not decode decisions: no statistics
         try:
@@ -477,6 +508,12 @@ class BatchDecodeEngine:
         finally:
             self._in_prefill = False
         return res
+
+    def match_path(self, P=None) -> int:
+        """mac_match_path of a parameter set (default: the last step's): which scan, verify layout
+        and amend the library launches for it (MAC_PATH_* bits, split-band items << 8)."""
+        P = P if P is not None else self.last_params
+        return int(_lib.load().mac_match_path(P))
 
     def _choose_match_mode(self):
         """The step's match scan (MacDecodeParams.match_mode), fixed for all of its stages."""
@@ -496,15 +533,20 @@ class BatchDecodeEngine:
         """Launch one stage (mac_append_kv | mac_match | mac_amend | mac_complete) — for profiling/tests."""
         self._layer(layer)
         if name == "mac_append_kv":  # a step's first stage: its match scan is chosen here
+            self._ensure_room(layer)
             self._choose_match_mode()
         dt = self._check_inputs(q_pre, k_pre, v)
         _lib.call(name, self._params(layer, q_pre, k_pre, v, dt, force_miss), self._stream())
+        if name == "mac_complete":  # the step's last stage advances seq_lens
+            self._len[layer] += 1
 
     def full_decode(self, layer: int, q_pre, k_pre, v) -> torch.Tensor:
         """Full-attention decode (append + exact attention over [1, m]): the baseline; no ring work."""
         self._layer(layer)
         dt = self._check_inputs(q_pre, k_pre, v)
+        self._ensure_room(layer)
         _lib.call("mac_full_decode", self._params(layer, q_pre, k_pre, v, dt, True), self._stream())
+        self._len[layer] += 1
         return self.o_out
 
     def attend_full(self, layer: int, q_pre) -> torch.Tensor:
@@ -548,6 +590,7 @@ class BatchDecodeEngine:
         self.ring_acc[layer][:, :, slots] = ring_acc.to(self.device, self.sumdt)
         self.ring_lse[layer][:, :, slots] = ring_lse.to(self.device, self.sumdt)
         self.seq_lens[layer].fill_(L)
+        self._len[layer] = L
         self.sync_ring_qp(layer)
 
     def sync_ring_qp(self, layer: int):
@@ -625,15 +668,37 @@ class StepGraph:
         # bf16 d = 128 engine with a bf16 output: no I/O kernels at all (see _body)
         self.direct = (cfg.storage == "bf16" and cfg.d == 128 and cfg.d_v == 128 and
                        self.out_dtype == torch.bfloat16)
-        self.graph = torch.cuda.CUDAGraph()
         self.h2d_bytes = self.in_host.numel() * self.in_host.element_size()
         self.d2h_bytes = self.out_host.numel() * self.out_host.element_size()
+        # A graph pins the kernels it captured, so the match scan (MacDecodeParams.match_mode) is
+        # fixed per graph: an adaptive engine whose geometry runs the two-pass scan gets one graph
+        # per scan and replay() picks one from the engine's misses feedback, like decode_step.
+        modes = [eng._step_mode]
+        if eng.match_mode == "adaptive":
+            P = eng._params(self.layers[0], eng.o_out, eng.o_out, eng.o_out, _lib.DT_BF16)
+            P.match_mode = 0
+            two = _lib.load().mac_match_path(P)
+            modes = [0, 1] if two > 0 and two & _lib.PATH_TWO_PASS else [0]
+        elif eng.match_mode == "one_pass":
+            modes = [1]
+        else:
+            modes = [0]
+        self.graphs = {}
+        saved = eng._step_mode
         s = torch.cuda.Stream(device=dev)
         s.wait_stream(torch.cuda.current_stream(dev))
-        # thread-local capture: the launchers' one-time setup (function attributes, occupancy
-        # queries) is not a stream operation and may run during the first capture
-        with torch.cuda.graph(self.graph, stream=s, capture_error_mode="thread_local"):
-            self._body()
+        try:
+            for mode in modes:
+                eng._step_mode = mode
+                g = torch.cuda.CUDAGraph()
+                # thread-local capture: the launchers' one-time setup (function attributes, occupancy
+                # queries) is not a stream operation and may run during the first capture
+                with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                    self._body()
+                self.graphs[mode] = g
+        finally:
+            eng._step_mode = saved
+        self.graph = self.graphs[modes[0]]
 
     def _io(self, src: int, src_dt: int, dst: int, dst_dt: int, n: int):
         lib = _lib.load()
@@ -659,7 +724,7 @@ class StepGraph:
                  self.in_host.numel())
         for i, lay in enumerate(self.layers):
             q, k, v = self._qkv_dev[i]
-            eng.decode_step(lay, q, k, v)
+            eng._decode_step_ptrs(lay, q.data_ptr(), k.data_ptr(), v.data_ptr(), dt[q.dtype])
             if self.multi:  # each layer's output leaves before the next layer reuses o_out
                 self._io(eng.o_out.data_ptr(), dt[eng.o_out.dtype], self._out_alias.value + i * per_out * osz,
                          dt[self.out_dtype], per_out)
@@ -667,7 +732,17 @@ class StepGraph:
             self._io(eng.o_out.data_ptr(), dt[eng.o_out.dtype], self._out_alias.value, dt[self.out_dtype], per_out)
 
     def replay(self):
+        """One step of every captured layer.  Raises ValueError (before launching) when a layer's
+        next position has no KV page: a graph cannot grow the pool (reserve() before capture)."""
+        eng = self.eng
+        for lay in self.layers:
+            eng._ensure_room(lay, grow=False)
+        if len(self.graphs) > 1:
+            eng._choose_match_mode()
+            self.graph = self.graphs.get(eng._step_mode, self.graph)
         self.graph.replay()
+        for lay in self.layers:
+            eng._len[lay] += 1
 
 
 # ----------------------------------------------------------------------------

@@ -139,6 +139,7 @@ class ShardedDecodeEngine:
         eng = self.engine
         eng._layer(layer)
         dt = eng._check_inputs(q_pre, k_pre, v)
+        eng._ensure_room(layer)
         _lib.call("mac_shard_partial", eng._params(layer, q_pre, k_pre, v, dt), eng._stream())
         return eng.shard_send
 
@@ -147,6 +148,7 @@ class ShardedDecodeEngine:
         eng = self.engine
         dt = eng._check_inputs(q_pre, k_pre, v)
         _lib.call("mac_shard_complete", eng._params(layer, q_pre, k_pre, v, dt), eng._stream())
+        eng._len[layer] += 1
         return eng.result()
 
     def decode_step(self, layer: int, q_pre, k_pre, v) -> BatchStepResult:

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 import mac_oracle as orc  # noqa: E402
 from golden_util import bf16_round, rel_err  # noqa: E402
 
-TOL = 2e-4
+TOL = 1e-4
 
 
 def _fast_path_used(eng):

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 import mac_oracle as orc  # noqa: E402
 from golden_util import bf16_round, rel_err  # noqa: E402
 
-TOL = 2e-4
+TOL = 1e-4
 
 
 def _setup(world, hq=8, hkv=2, W=64, r=16, n0=3000, S=6, rep_prob=0.6, seed=7):
