@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 7
+#define MACATTN_ABI_VERSION 8
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -206,6 +206,17 @@ size_t mac_workspace_bytes(const MacDecodeParams* p);
 size_t mac_overflow_flag_offset(const MacDecodeParams* p);
 /* which kernel family mac_amend would launch: 0 generic CUDA-core, 1 bf16 tensor-core (mma) */
 int mac_amend_variant(const MacDecodeParams* p);
+
+/* which kernels mac_decode_step launches for this parameter set (host-side decision, no launch):
+ * a bit set of MAC_PATH_* plus, in bits 8-15, the split-band items per GQA group (0: the band
+ * rides in the plan); -1 for an invalid parameter set.  Tests use it to prove which path ran. */
+enum {
+  MAC_PATH_TWO_PASS = 1,      /* two-pass match: planar scan + verify kernel */
+  MAC_PATH_VERIFY_GROUP = 2,  /* verify: one CTA per GQA group */
+  MAC_PATH_VERIFY_HEAD = 4,   /* verify: one CTA per head */
+  MAC_PATH_AMEND_MMA = 8      /* bf16 d = 128 tensor-core amend (else the generic CUDA-core amend) */
+};
+int mac_match_path(const MacDecodeParams* p);
 
 int mac_append_kv(const MacDecodeParams* p, void* stream);
 int mac_match(const MacDecodeParams* p, void* stream);

@@ -13,13 +13,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
 MATCH_PRE_ROPE, MATCH_POST_ROPE = 0, 1
 DOWNDATE_SPLIT, DOWNDATE_REMOVE = 0, 1
+PATH_TWO_PASS, PATH_VERIFY_GROUP, PATH_VERIFY_HEAD, PATH_AMEND_MMA = 1, 2, 4, 8
 
 EXPORTS = (
     "mac_abi_version",
@@ -28,6 +29,7 @@ EXPORTS = (
     "mac_workspace_bytes",
     "mac_overflow_flag_offset",
     "mac_amend_variant",
+    "mac_match_path",
     "mac_append_kv",
     "mac_match",
     "mac_match_scan",
@@ -169,6 +171,8 @@ def load() -> C.CDLL:
     lib.mac_overflow_flag_offset.argtypes = [C.POINTER(MacDecodeParams)]
     lib.mac_amend_variant.restype = C.c_int
     lib.mac_amend_variant.argtypes = [C.POINTER(MacDecodeParams)]
+    lib.mac_match_path.restype = C.c_int
+    lib.mac_match_path.argtypes = [C.POINTER(MacDecodeParams)]
     for name in ("mac_append_kv", "mac_match", "mac_match_scan", "mac_match_verify", "mac_amend", "mac_complete", "mac_decode_step", "mac_full_decode",
                  "mac_attend_full", "mac_shard_partial", "mac_shard_complete"):
         fn = getattr(lib, name)

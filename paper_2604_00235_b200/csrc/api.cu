@@ -133,6 +133,18 @@ int mac_amend_variant(const MacDecodeParams* p) {
   return (p && p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) ? 1 : 0;
 }
 
+int mac_match_path(const MacDecodeParams* p) {
+  if (!p || validate(p, false)) return -1;
+  int path = 0;
+  if (p->storage == MAC_MODE_BF16 && match_fast_supported(*p) && front_two_pass(*p)) {
+    path |= MAC_PATH_TWO_PASS;
+    path |= verify_per_group(*p) ? MAC_PATH_VERIFY_GROUP : MAC_PATH_VERIFY_HEAD;
+  }
+  if (p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) path |= MAC_PATH_AMEND_MMA;
+  const int nb = (p->storage == MAC_MODE_BF16) ? band_split(*p) : 0;
+  return path | (nb << 8);
+}
+
 int mac_append_kv(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_APPEND, false); }
 int mac_match(const MacDecodeParams* p, void* stream) { return dispatch(p, stream, STAGE_MATCH, true); }
 int mac_match_scan(const MacDecodeParams* p, void* stream) {

@@ -401,6 +401,7 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
 // host-side path decisions shared by the launchers (match_fast.cu, amend_mma.cu)
 bool match_fast_supported(const MacDecodeParams& p);
 bool front_two_pass(const MacDecodeParams& p);
+bool verify_per_group(const MacDecodeParams& p);
 bool amend_mma_supported(const MacDecodeParams& p);
 int band_split(const MacDecodeParams& p);
 int piece_target(const MacDecodeParams& p);
