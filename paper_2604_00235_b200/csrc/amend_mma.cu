@@ -17,6 +17,10 @@ namespace mac {
 __device__ unsigned long long g_amend_trace[4096 * 8];
 #endif
 
+bool amend_tma_supported(const MacDecodeParams& p);
+int amend_tma_grid(cudaError_t* err);
+cudaError_t launch_amend_tma(const MacDecodeParams& p, cudaStream_t st, int nb);
+
 bool amend_mma_supported(const MacDecodeParams& p) {
   const int g = p.n_q_heads / p.n_kv_heads;
   return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128 && g >= 1 && g <= 8 &&
@@ -158,6 +162,21 @@ static int amend_grid_full(int vi, cudaError_t* err) {
 // one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
 // (1..4).  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
 // kernel's plan and this launch call it with the same parameters, so they always agree.
+// The hit step's amend runs on the TMA kernel (amend_tma.cu) unless the KV is sharded or the
+// tensor-map encoder is unavailable; development builds can force the one-warp kernel with
+// MAC_AMEND_TMA=0.
+static bool hit_amend_tma(const MacDecodeParams& p) {
+#ifdef MAC_DEV_KNOBS
+  static int forced = -2;
+  if (forced == -2) {
+    const char* env = getenv("MAC_AMEND_TMA");
+    forced = env ? atoi(env) : -1;
+  }
+  if (forced == 0) return false;
+#endif
+  return p.n_shards == 0 && amend_tma_supported(p);
+}
+
 int band_split(const MacDecodeParams& p) {
 #ifdef MAC_DEV_KNOBS
   static int forced = -2;
@@ -171,16 +190,24 @@ int band_split(const MacDecodeParams& p) {
   if (forced == 0 || !amend_mma_supported(p) || !front_two_pass(p) || p.kv_offset != 0 || p.kv_limit != 0 ||
       p.band <= 0)
     return 0;
-  int nb = forced > 0 ? forced : amend_grid_full(amend_variant(false), nullptr) / (p.batch * p.n_kv_heads);
+  const int G = p.batch * p.n_kv_heads;
+  int nb = forced > 0 ? forced
+                      : (hit_amend_tma(p) ? (amend_tma_grid(nullptr) + G - 1) / G
+                                          : amend_grid_full(amend_variant(false), nullptr) / G);
   if (nb > 4 && forced < 0) nb = 4;
   if (nb > p.max_chunks - 1) nb = p.max_chunks - 1;
   return nb < 1 ? 0 : nb;
 }
 
 // piece items per group with the split band: the persistent grid's warps per group (>= 1)
+// (encoded for plan_chunking: the TMA amend's CTAs take items of up to 512 tokens, two per CTA)
 int piece_target(const MacDecodeParams& p) {
-  const int t = amend_grid_full(amend_variant(false), nullptr) /
-                (p.batch * p.n_kv_heads);
+  const int G = p.batch * p.n_kv_heads;
+  if (hit_amend_tma(p)) {
+    const int t = 2 * amend_tma_grid(nullptr) / G;
+    return (t < 1 ? 1 : (t > 0xffff ? 0xffff : t)) | (32 << 16);
+  }
+  const int t = amend_grid_full(amend_variant(false), nullptr) / G;
   return t < 1 ? 1 : t;
 }
 
@@ -193,6 +220,7 @@ cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, boo
   const int gfull = amend_grid_full(vi, &err);
   if (err != cudaSuccess) return err;
   const int nb = full_spans ? 0 : band_split(p);
+  if (!full_spans && hit_amend_tma(p)) return launch_amend_tma(p, st, nb);
   const long cap = (long)p.batch * p.n_kv_heads * p.max_chunks;
   const int grid = (int)(gfull < cap ? gfull : cap);
   // programmatic dependent launch: the grid is set up while the front kernel drains

@@ -84,6 +84,15 @@ __device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
 }
 // byte offset of 16-byte chunk `c` (0..15) of row `r` in a swizzled 16 x 256 B tile
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 256 + ((c ^ (r & 7)) << 4)); }
+// the same tile as the TMA engine writes it with CU_TENSOR_MAP_SWIZZLE_128B and 64-dim boxes
+// (amend_tma.cu): two 16 x 128 B halves (dims 0..63, 64..127), the 16-byte chunk index XORed
+// with the row's low 3 bits inside each 128 B row (tile base 1024-byte aligned)
+__device__ __forceinline__ uint32_t swz128(int r, int c) {
+  return (uint32_t)(((c >> 3) << 11) + (r << 7) + (((c & 7) ^ (r & 7)) << 4));
+}
+template <bool SW128> __device__ __forceinline__ uint32_t tile_off(int r, int c) {
+  return SW128 ? swz128(r, c) : swz(r, c);
+}
 
 struct State {
   float o[16][4];
@@ -99,7 +108,7 @@ struct State {
 
 // fold one 32-token step (two 16-token sub-tiles; this lane: 8 tokens of head `row`)
 // into the online-softmax state and accumulate P V.  vs1 == 0: second sub-tile absent.
-template <bool HAS1>
+template <bool HAS1, bool SW128 = false>
 __device__ __forceinline__ void softmax_pv(State& S, const float* l_in, const int* tok, int lo, int hi,
                                            uint32_t vs0, uint32_t vs1, int lane) {
   float l[8];
@@ -150,12 +159,12 @@ __device__ __forceinline__ void softmax_pv(State& S, const float* l_in, const in
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     uint32_t b0, b1, b2, b3;
-    ldsm_x4_t(vs0 + swz(trow, 2 * j + (mi >> 1)), b0, b1, b2, b3);
+    ldsm_x4_t(vs0 + tile_off<SW128>(trow, 2 * j + (mi >> 1)), b0, b1, b2, b3);
     mma16816(S.o[2 * j], pa[0], b0, b1);
     mma16816(S.o[2 * j + 1], pa[0], b2, b3);
     if (HAS1) {  // compile-time: no predicated ldmatrix (which costs a WARPSYNC + NOP each)
       uint32_t c0, c1, c2, c3;
-      ldsm_x4_t(vs1 + swz(trow, 2 * j + (mi >> 1)), c0, c1, c2, c3);
+      ldsm_x4_t(vs1 + tile_off<SW128>(trow, 2 * j + (mi >> 1)), c0, c1, c2, c3);
       mma16816(S.o[2 * j], pa[1], c0, c1);
       mma16816(S.o[2 * j + 1], pa[1], c2, c3);
     }

@@ -210,9 +210,12 @@ __host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams
   const int span = m - p.band - grid_start(lo_g, p.kv_offset) + 1;
   if (span <= 0) return chunking(span, 1, 16);
   const int cap = p.max_chunks - nb;
+  // ntarget: bits 0-15 the item count target, bits 16+ the longest item in 16-token sub-tiles
+  // (0: 256 tokens, the one-warp amend; the CTA-cooperative TMA amend streams longer items)
+  const int tgt = ntarget & 0xffff, max_len = (ntarget >> 16) > 0 ? (ntarget >> 16) * 16 : 256;
   int n = (span + p.min_chunk - 1) / p.min_chunk;
-  if (ntarget > 0 && n > ntarget) n = ntarget;
-  const int n_len = (span + 255) / 256;
+  if (tgt > 0 && n > tgt) n = tgt;
+  const int n_len = (span + max_len - 1) / max_len;
   if (n < n_len) n = n_len;
   if (n > cap) n = cap;
   if (n < 1) n = 1;
