@@ -33,6 +33,15 @@
  *   mac_mass_bound    mass_bound_check (engine.py:246-281), offline, over the
  *                     paged cache
  *
+ * The reference's public building blocks on plain device arrays (f64 math):
+ *   mac_summarize     summarize / attend_full (attention.py:75-116,182-189) for many
+ *                     query rows, each over its own key range, q optionally rotated
+ *                     at t first: also the batched causal oracle_outputs
+ *                     (engine.py:542-572)
+ *   mac_remove_summaries  remove() and its guards (attention.py:138-172)
+ *   mac_rope_rotate   rope_rotate (attention.py:212-232)
+ *   mac_match_rows    match_query (matching.py:141-175) over QueryRing arrays
+ *
  * Conventions: plain device pointers and sizes, no allocation inside, every
  * launch is stream-ordered and graph-capturable (no host synchronisation).
  * Return value 0 on success, a MAC_ERR_* code for a rejected parameter set,
@@ -48,7 +57,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 8
+#define MACATTN_ABI_VERSION 9
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -196,6 +205,49 @@ typedef struct MacMassBoundParams {
   double* out;                  /* [n, 2] (lhs, rhs) of engine.py:246-281 */
 } MacMassBoundParams;
 
+/* summarize (attention.py:75-116) for n_sets * q_per_set query rows.  Query set s reads key
+ * set s / sets_per_kv (GQA); row i of a set covers keys [lo, hi] (1-based, inclusive; an
+ * empty range gives the empty summary acc = 0, lse = -inf).  Scale 1/sqrt(head_dim). */
+typedef struct MacSummarizeParams {
+  int32_t n_sets;
+  int32_t q_per_set;
+  int32_t n_keys;           /* rows per key set */
+  int32_t sets_per_kv;      /* query sets per key set (>= 1) */
+  int32_t head_dim;         /* d, even, <= 1024 */
+  int32_t head_dim_v;       /* d_v <= 256 */
+  int32_t dtype;            /* MAC_DT_F32 | MAC_DT_F64 of q / keys / values */
+  const void* q;            /* [n_sets, q_per_set, d] */
+  const void* keys;         /* [n_sets / sets_per_kv, n_keys, d] */
+  const void* values;       /* [n_sets / sets_per_kv, n_keys, d_v] */
+  const int32_t* lo;        /* optional [n_sets * q_per_set] first key; NULL: 1 */
+  const int32_t* hi;        /* optional [n_sets * q_per_set] last key; NULL: n_keys */
+  const int32_t* rope_t;    /* optional [n_sets * q_per_set]: rotate q at this position first */
+  const double* rope_freqs; /* [d/2], needed with rope_t */
+  double* out_acc;          /* [n_sets * q_per_set, d_v] */
+  double* out_lse;          /* [n_sets * q_per_set] */
+} MacSummarizeParams;
+
+/* match_query (matching.py:141-175) for n_rings independent rings of explicit positions. */
+typedef struct MacMatchRowsParams {
+  int32_t n_rings;
+  int32_t capacity;         /* rows per ring (stride) */
+  int32_t head_dim;
+  int32_t delta_max;        /* <= 0: off */
+  int32_t post_rope;        /* 1: candidates rotated by R(pos - m) first (matching.py:165-168) */
+  double thr_sq;            /* threshold(d, tau)^2; hit iff best < thr_sq */
+  const double* rope_freqs; /* [d/2], needed with post_rope */
+  const double* q;          /* [n_rings, d] */
+  const double* ring_q;     /* [n_rings, capacity, d] */
+  const double* ring_sqnorm;/* [n_rings, capacity] cached |c|^2 (matching.py:109) */
+  const int64_t* ring_pos;  /* [n_rings, capacity] */
+  const int32_t* n_live;    /* [n_rings] live rows (the first n_live of each ring) */
+  const int32_t* m;         /* [n_rings] current position */
+  int32_t* out_hit;
+  int32_t* out_pos;         /* -1 on a miss */
+  double* out_dist;         /* +inf when nothing was scanned */
+  int32_t* out_scanned;
+} MacMatchRowsParams;
+
 int mac_abi_version(void);
 size_t mac_params_size(void);
 const char* mac_error_string(int code);
@@ -258,6 +310,18 @@ int mac_mass_bound(const MacDecodeParams* p, const MacMassBoundParams* mb, void*
  * n_elems * element size a multiple of 16 (of 8 elements when narrowing). */
 int mac_host_alias(void* host, void** device_alias);
 int mac_io_copy(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, size_t n_elems, void* stream);
+
+int mac_summarize(const MacSummarizeParams* p, void* stream);
+/* remove(a, band) row-wise in f64; status[row]: 0 ok, 1 CancellationError (|a.lse - band.lse|
+ * < eps_cancel), 2 MassExceededError (band.lse > a.lse + eps_cancel).  Token-count checks
+ * (attention.py:156-162) are the caller's. */
+int mac_remove_summaries(int32_t n_rows, int32_t head_dim_v, const double* a_acc, const double* a_lse,
+                         const double* band_acc, const double* band_lse, double eps_cancel, double* out_acc,
+                         double* out_lse, int32_t* status, void* stream);
+/* out[i] = R(t[i]) x[i] for n_rows rows of head_dim (interleaved pairs, f64 angles) */
+int mac_rope_rotate(int32_t n_rows, int32_t head_dim, const double* x, const double* t, const double* rope_freqs,
+                    double* out, void* stream);
+int mac_match_rows(const MacMatchRowsParams* p, void* stream);
 
 #ifdef __cplusplus
 }

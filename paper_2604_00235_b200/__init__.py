@@ -37,17 +37,32 @@ from .workload import PRESETS, SyntheticSpec, Trace, TraceError, gen_synthetic, 
 __version__ = "0.1.0"
 
 
-def __getattr__(name):
-    # the device engines import torch; load them on first use
-    if name in ("BatchDecodeEngine", "BatchStepResult", "DecodeEngine", "StepGraph", "run_decode", "KvStoreView",
-                "QueryRingView", "SummaryRingView", "TrafficCounter", "rope_freqs", "mass_bound_check"):
-        from . import engine
+_LAZY = {
+    # the device modules import torch; load them on first use
+    "engine": ("BatchDecodeEngine", "BatchStepResult", "DecodeEngine", "StepGraph", "run_decode", "oracle_outputs",
+               "KvStoreView", "QueryRingView", "SummaryRingView", "rope_freqs", "mass_bound_check"),
+    "summary": ("RopeTable", "attend_full", "avg_cos", "merge", "remove", "rope_rotate", "summarize",
+                "summarize_rows", "rope_rotate_rows"),
+    "rings": ("QueryRing", "SummaryRing", "match_query", "match_queries"),
+    "store": ("KvPage", "KvStore", "TrafficCounter"),
+}
 
-        return getattr(engine, name)
+
+def __getattr__(name):
+    import importlib
+
+    for mod, names in _LAZY.items():
+        if name in names:
+            return getattr(importlib.import_module(f".{mod}", __name__), name)
     raise AttributeError(name)
 
 
+# the reference's public names on the decode path (attnreuse/__init__.py:3-65) minus the
+# out-of-scope offline scheduler (sched.py) and tau calibration (calibrate_tau, chi2_cdf),
+# plus this package's batched device API
 __all__ = [
+    "KvPage", "KvStore", "QueryRing", "RopeTable", "SummaryRing", "attend_full", "avg_cos", "match_queries",
+    "match_query", "merge", "oracle_outputs", "remove", "rope_rotate", "summarize",
     "AttentionSummary", "BatchDecodeEngine", "BatchStepResult", "ByteCostModel", "CancellationError",
     "DOWNDATE_REMOVE", "DOWNDATE_SPLIT", "DecodeEngine", "DecodeMetrics", "EmptySummaryError", "EngineConfig",
     "MATCH_POST_ROPE", "MATCH_PRE_ROPE", "MassExceededError", "MatchConfig", "MatchResult", "PRESETS",

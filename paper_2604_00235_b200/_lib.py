@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -47,6 +47,10 @@ EXPORTS = (
     "mac_mass_bound",
     "mac_host_alias",
     "mac_io_copy",
+    "mac_summarize",
+    "mac_remove_summaries",
+    "mac_rope_rotate",
+    "mac_match_rows",
 )
 
 # per-head / per-group statistics fields of mac_step_stats (include/macattn.h)
@@ -144,6 +148,49 @@ class MacMassBoundParams(C.Structure):
     ]
 
 
+class MacSummarizeParams(C.Structure):
+    _fields_ = [
+        ("n_sets", C.c_int32),
+        ("q_per_set", C.c_int32),
+        ("n_keys", C.c_int32),
+        ("sets_per_kv", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("head_dim_v", C.c_int32),
+        ("dtype", C.c_int32),
+        ("q", C.c_void_p),
+        ("keys", C.c_void_p),
+        ("values", C.c_void_p),
+        ("lo", C.c_void_p),
+        ("hi", C.c_void_p),
+        ("rope_t", C.c_void_p),
+        ("rope_freqs", C.c_void_p),
+        ("out_acc", C.c_void_p),
+        ("out_lse", C.c_void_p),
+    ]
+
+
+class MacMatchRowsParams(C.Structure):
+    _fields_ = [
+        ("n_rings", C.c_int32),
+        ("capacity", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("delta_max", C.c_int32),
+        ("post_rope", C.c_int32),
+        ("thr_sq", C.c_double),
+        ("rope_freqs", C.c_void_p),
+        ("q", C.c_void_p),
+        ("ring_q", C.c_void_p),
+        ("ring_sqnorm", C.c_void_p),
+        ("ring_pos", C.c_void_p),
+        ("n_live", C.c_void_p),
+        ("m", C.c_void_p),
+        ("out_hit", C.c_void_p),
+        ("out_pos", C.c_void_p),
+        ("out_dist", C.c_void_p),
+        ("out_scanned", C.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -190,6 +237,14 @@ def load() -> C.CDLL:
     lib.mac_io_copy.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_size_t, C.c_void_p]
     lib.mac_merge_partials.restype = C.c_int
     lib.mac_merge_partials.argtypes = [C.POINTER(MacMergeParams), C.c_void_p]
+    lib.mac_summarize.restype = C.c_int
+    lib.mac_summarize.argtypes = [C.POINTER(MacSummarizeParams), C.c_void_p]
+    lib.mac_match_rows.restype = C.c_int
+    lib.mac_match_rows.argtypes = [C.POINTER(MacMatchRowsParams), C.c_void_p]
+    lib.mac_remove_summaries.restype = C.c_int
+    lib.mac_remove_summaries.argtypes = [C.c_int32, C.c_int32] + [C.c_void_p] * 4 + [C.c_double] + [C.c_void_p] * 4
+    lib.mac_rope_rotate.restype = C.c_int
+    lib.mac_rope_rotate.argtypes = [C.c_int32, C.c_int32] + [C.c_void_p] * 5
     if lib.mac_abi_version() != ABI_VERSION:
         raise RuntimeError(f"libmacattn ABI {lib.mac_abi_version()} != expected {ABI_VERSION}; rebuild")
     if lib.mac_params_size() != C.sizeof(MacDecodeParams):

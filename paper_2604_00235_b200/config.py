@@ -44,6 +44,12 @@ class AttentionSummary:
     lse: float
     count: int
 
+    def astype(self, dtype) -> "AttentionSummary":
+        """The summary as stored in `dtype` (acc and a finite lse rounded through it)."""
+        dt = np.dtype(dtype)
+        lse = self.lse if math.isinf(self.lse) else float(dt.type(self.lse))
+        return AttentionSummary(acc=self.acc.astype(dt), lse=lse, count=self.count)
+
 
 def empty_summary(d_v: int, dtype=np.float64) -> AttentionSummary:
     return AttentionSummary(acc=np.zeros(d_v, dtype=dtype), lse=-math.inf, count=0)

@@ -30,6 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .store import KvPage, TrafficCounter
 from .config import (
     DOWNDATE_REMOVE,
     MATCH_POST_ROPE,
@@ -758,7 +759,7 @@ class QueryRingView:
         self.d = eng.cfg.d
 
     def _count(self) -> int:
-        return int(self._e._n[self._l])
+        return int(self._e._ring_last[self._l, self._h])
 
     def __len__(self):
         return min(self._count(), self.capacity)
@@ -812,28 +813,13 @@ class SummaryRingView:
         return AttentionSummary(acc=acc, lse=lse, count=max(0, pos - self._e.cfg.band))
 
 
-class TrafficCounter:
-    """Logical KV read traffic (kvstore.py:19-30), folded from the device decisions."""
-
-    def __init__(self):
-        from collections import Counter
-
-        self.tokens_read = 0
-        self.bytes_read = 0
-        self.read_histogram = Counter()
-
-    def record(self, tokens: int, nbytes: int):
-        self.tokens_read += tokens
-        self.bytes_read += nbytes
-        self.read_histogram[tokens.bit_length()] += 1
-
-
 class KvStoreView:
     """Host view of the paged device KV cache with the KvStore read API (kvstore.py:62-165)."""
 
-    def __init__(self, eng: "DecodeEngine"):
+    def __init__(self, eng: "DecodeEngine", page_rounded_bytes: bool = False):
         self._e = eng
         self.d, self.d_v, self.page_size = eng.cfg.d, eng.cfg.d_v, eng.cfg.page_size
+        self.page_rounded_bytes = page_rounded_bytes
 
     @property
     def token_bytes(self) -> int:
@@ -856,11 +842,31 @@ class KvStoreView:
         keys = b.k_cache[layer][pages, kv_head, slots].double().cpu().numpy()
         vals = b.v_cache[layer][pages, kv_head, slots].double().cpu().numpy()
         if counter is not None:
-            counter.record(hi - lo + 1, (hi - lo + 1) * self.token_bytes)
+            tokens = hi - lo + 1
+            if self.page_rounded_bytes:  # kvstore.py:137-140
+                n_pages = (hi - 1) // self.page_size - (lo - 1) // self.page_size + 1
+                counter.record(tokens, n_pages * self.page_size * self.token_bytes)
+            else:
+                counter.record(tokens, tokens * self.token_bytes)
         return keys, vals
 
     def n_pages(self, layer: int, kv_head: int) -> int:
         return -(-self.length(layer, kv_head) // self.page_size)
+
+    def page(self, layer: int, kv_head: int, index: int) -> KvPage:
+        """Page `index` of (layer, kv head) from the paged device cache (kvstore.py:150-165):
+        page_size rows, zero beyond the stored tokens."""
+        n_pages = self.n_pages(layer, kv_head)
+        if not 0 <= index < n_pages:
+            raise IndexError(f"page {index} out of range ({n_pages} pages)")
+        b = self._e.batch
+        phys = int(b.page_table[0, index].item())
+        fill = min(self.length(layer, kv_head) - index * self.page_size, self.page_size)
+        keys = b.k_cache[layer][phys, kv_head].double().cpu().numpy()
+        vals = b.v_cache[layer][phys, kv_head].double().cpu().numpy()
+        keys[fill:] = 0.0
+        vals[fill:] = 0.0
+        return KvPage(keys=keys, values=vals, fill=fill)
 
 
 class DecodeEngine:
@@ -876,7 +882,42 @@ class DecodeEngine:
         self.oracle_traffic = TrafficCounter()
         self.store = KvStoreView(self)
         self._n = [0] * cfg.n_layers
+        # last ring position per (layer, head): the engine's step writes every head's slot, a
+        # caller's rectify_append one head's
+        self._ring_last = np.zeros((cfg.n_layers, cfg.n_q_heads), dtype=np.int64)
         self._group = cfg.n_q_heads // cfg.n_kv_heads
+
+    def rectify_append(self, layer: int, head: int, m: int, q_pre, full: AttentionSummary, band: AttentionSummary,
+                       prefix: AttentionSummary):
+        """Push (q_pre, prefix) as the (layer, head) ring entry of position m (engine.py:374-402):
+        the same count checks and storage rounding, written into ring slot (m - 1) % W of the
+        device rings (and the planar copy the two-pass scan reads).  The device rings are
+        slot-aligned, so m must follow the ring's last position by exactly one."""
+        cfg = self.cfg
+        if full.count != m:
+            raise ValueError(f"full summary covers {full.count} tokens, expected {m}")
+        if prefix.count != max(0, m - cfg.band):
+            raise ValueError(f"prefix summary covers {prefix.count} tokens, expected {max(0, m - cfg.band)}")
+        if not 0 <= layer < cfg.n_layers or not 0 <= head < cfg.n_q_heads:
+            raise ValueError(f"(layer, head) = ({layer}, {head}) out of range")
+        last = int(self._ring_last[layer, head])
+        if m <= last:
+            raise ValueError(f"ring positions must increase: got {m} after {last}")
+        if m != last + 1:
+            raise ValueError(f"device rings are slot-aligned: position {m} must follow {last} directly")
+        q = np.asarray(q_pre, dtype=np.float64)
+        if q.shape != (cfg.d,):
+            raise ValueError(f"expected query of dim {cfg.d}, got shape {q.shape}")
+        b = self.batch
+        slot = (m - 1) % cfg.window
+        b.ring_q[layer][0, head, slot] = torch.from_numpy(q).to(self.device, b.ring_q[layer].dtype)
+        b.ring_acc[layer][0, head, slot] = torch.from_numpy(np.asarray(prefix.acc, dtype=np.float64)).to(
+            self.device, b.ring_acc[layer].dtype)
+        b.ring_lse[layer][0, head, slot] = float(prefix.lse)
+        if b.ring_qp is not None:
+            b.ring_qp[layer][0, head, slot] = b.ring_q[layer][0, head, slot, :_lib.PLANAR_DIMS].to(
+                b.ring_qp[layer].dtype)
+        self._ring_last[layer, head] = m
 
     def rings(self, layer: int, head: int):
         return QueryRingView(self, layer, head), SummaryRingView(self, layer, head)
@@ -895,6 +936,8 @@ class DecodeEngine:
             raise ValueError(f"layer {layer} out of range")
         if m != self._n[layer] + 1:
             raise ValueError(f"steps must be consecutive: store is at {self._n[layer] + 1}, step is {m}")
+        if int(self._ring_last[layer].max()) >= m:
+            raise ValueError(f"ring positions must increase: got {m} after {int(self._ring_last[layer].max())}")
         self.batch.reserve(m)
         dev = self.device
         q = torch.from_numpy(q_pre).to(dev)[None].contiguous()
@@ -909,6 +952,7 @@ class DecodeEngine:
             ("dist", res.match_dist), ("scan", res.match_scanned), ("flse", res.full_lse),
             ("rho", res.band_mass), ("cacc", res.cached_acc), ("clse", res.cached_lse), ("fb", res.fallbacks))}
         self._n[layer] = m
+        self._ring_last[layer] = m
         ref_rows = None
         if cfg.oracle_mode:
             if oracle_rows is not None:
@@ -976,17 +1020,55 @@ class DecodeEngine:
                           errs=tuple(errs) if errs is not None else None, delta=delta)
 
 
+def oracle_outputs(trace, cfg: EngineConfig, *, chunk: int = 256, device="cuda") -> np.ndarray:
+    """Exact causal attention outputs for every (layer, step, q head) of a trace
+    (engine.py:542-572), batched on the device: keys rotated at their positions and rounded
+    through the storage dtype exactly as the engine stores them, query t rotated at t and
+    attended over keys [1, t] in f64 (mac_rope_rotate + mac_summarize, one summarize launch
+    per layer).  Returns (n_layers, L, n_q_heads, d_v) f64; `chunk` bounds the query rows of
+    one launch."""
+    from .summary import rope_rotate_rows, summarize_rows
+
+    dev = torch.device(device)
+    L, Hq, Hkv, d, dv = int(trace.seq_len), cfg.n_q_heads, cfg.n_kv_heads, cfg.d, cfg.d_v
+    g = Hq // Hkv
+    freqs = torch.from_numpy(rope_freqs(d, cfg.rope_base)).to(dev)
+    pos = torch.arange(1, L + 1, dtype=torch.float64, device=dev)
+    out = np.empty((cfg.n_layers, L, Hq, dv), dtype=np.float64)
+    store = {"f32": torch.float32, "bf16": torch.bfloat16, "f64": torch.float64}[cfg.storage]
+    for layer in range(cfg.n_layers):
+        k = torch.from_numpy(np.ascontiguousarray(trace.k_pre[:, layer], dtype=np.float64)).to(dev)  # [L, Hkv, d]
+        v = torch.from_numpy(np.ascontiguousarray(trace.v[:, layer], dtype=np.float64)).to(dev)
+        k_rot = rope_rotate_rows(k.permute(1, 0, 2).reshape(Hkv * L, d), pos.repeat(Hkv), freqs).view(Hkv, L, d)
+        vv = v.permute(1, 0, 2).contiguous()
+        k_rot, vv = k_rot.to(store).double(), vv.to(store).double()  # storage rounding
+        q = torch.from_numpy(np.ascontiguousarray(trace.q_pre[:, layer], dtype=np.float64)).to(dev)
+        q = q.permute(1, 0, 2).contiguous()  # [Hq, L, d]
+        step = max(1, int(chunk))
+        for lo in range(0, L, step):
+            hi = min(L, lo + step)
+            t = torch.arange(lo + 1, hi + 1, dtype=torch.int32, device=dev).expand(Hq, hi - lo).contiguous()
+            acc, _ = summarize_rows(q[:, lo:hi], k_rot[:, :hi], vv[:, :hi], hi=t, rope_t=t, rope_freqs=freqs,
+                                    sets_per_kv=g)
+            out[layer, lo:hi] = acc.permute(1, 0, 2).cpu().numpy()
+    return out
+
+
 def run_decode(trace, cfg: EngineConfig, *, per_step_oracle: bool = False, on_step=None,
                device="cuda") -> DecodeEngine:
-    """Drive a whole trace through a fresh engine (engine.py:575-607)."""
+    """Drive a whole trace through a fresh engine (engine.py:575-607).  With oracle_mode the
+    reference rows come from one batched device pass (oracle_outputs) unless per_step_oracle
+    is set, in which case every step computes its own (mac_attend_full on the stored cache)."""
     if (trace.d, trace.d_v, trace.n_layers, trace.n_q_heads, trace.n_kv_heads) != (
             cfg.d, cfg.d_v, cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads):
         raise ValueError("trace dimensions do not match the engine config")
     eng = DecodeEngine(cfg, device=device, capacity=int(trace.seq_len))
+    oracle = oracle_outputs(trace, cfg, device=eng.device) if cfg.oracle_mode and not per_step_oracle else None
     for m in range(1, int(trace.seq_len) + 1):
         for layer in range(cfg.n_layers):
+            rows = oracle[layer, m - 1] if oracle is not None else None
             res = eng.decode_step(layer, trace.q_pre[m - 1, layer], trace.k_pre[m - 1, layer],
-                                  trace.v[m - 1, layer], m)
+                                  trace.v[m - 1, layer], m, oracle_rows=rows)
             if on_step is not None:
                 on_step(m, layer, res)
     return eng

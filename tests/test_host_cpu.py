@@ -246,3 +246,45 @@ def test_algorithmic_step_bytes_by_hand():
     # a miss reads the group's whole context
     b2 = bench.step_bytes(np.array([[0, 1]]), pos, np.array([100]), hq=2, hkv=1, d=128, window=64, band=16)
     assert b2["amend"] == 100 * 2 * 128 * 2
+
+
+def test_public_names_cover_reference(golden_dir):
+    """Every public name of the reference package (attnreuse/__init__.py:3-65, recorded by
+    tests/golden/make_api_list.py) except the out-of-scope scheduler / calibration is exported,
+    and each resolves (the device modules import lazily; nothing here launches)."""
+    import json
+
+    import paper_2604_00235_b200 as pkg
+
+    with open(os.path.join(golden_dir, "reference_api.json")) as fh:
+        ref = json.load(fh)
+    want = set(ref["reference_all"]) - set(ref["out_of_scope"])
+    assert not want - set(pkg.__all__), sorted(want - set(pkg.__all__))
+    for name in pkg.__all__:
+        assert getattr(pkg, name) is not None, name
+
+
+def test_new_entry_points_validate_without_gpu():
+    """mac_summarize / mac_match_rows / mac_remove_summaries / mac_rope_rotate reject bad
+    parameter sets before any launch."""
+    import ctypes
+
+    from paper_2604_00235_b200 import _lib
+
+    lib = _lib.load()
+    s = _lib.MacSummarizeParams()
+    assert lib.mac_summarize(s, None) == 1001
+    buf = (ctypes.c_double * 16)()
+    a = ctypes.addressof(buf)
+    s.q = s.keys = s.values = s.out_acc = s.out_lse = a
+    assert lib.mac_summarize(s, None) == 1002  # sets_per_kv 0, head_dim 0
+    s.sets_per_kv, s.head_dim, s.head_dim_v, s.dtype = 1, 4, 4, 5
+    assert lib.mac_summarize(s, None) == 0  # zero rows: nothing to launch
+    s.n_sets = s.q_per_set = 1
+    assert lib.mac_summarize(s, None) == 1003  # unknown dtype
+    s.rope_t = a
+    assert lib.mac_summarize(s, None) == 1001  # rotation without frequencies
+    m = _lib.MacMatchRowsParams()
+    assert lib.mac_match_rows(m, None) == 1001
+    assert lib.mac_remove_summaries(1, 4, None, a, a, a, 1e-6, a, a, a, None) == 1001
+    assert lib.mac_rope_rotate(1, 3, a, a, a, a, None) == 1002
