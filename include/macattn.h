@@ -32,6 +32,9 @@
  *                     on the device per head after a step
  *   mac_mass_bound    mass_bound_check (engine.py:246-281), offline, over the
  *                     paged cache
+ *   mac_build_ring    the ring entries of the last n prompt positions from the
+ *                     cached KV in one GEMM-form pass (what n forced-miss decode steps
+ *                     write, engine.py:374-402 + 484-499)
  *
  * The reference's public building blocks on plain device arrays (f64 math):
  *   mac_summarize     summarize / attend_full (attention.py:75-116,182-189) for many
@@ -57,7 +60,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 9
+#define MACATTN_ABI_VERSION 10
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -152,8 +155,10 @@ typedef struct MacDecodeParams {
   size_t workspace_bytes;
   /* ---- match-scan choice (bf16 d = 128 path) ------------------------------ */
   int32_t match_mode;         /* 0: by geometry (two-pass scan + verify for rings of 512..1024 rows
-                                 and enough heads); 1: one-pass scan.  Both are exact: the choice
-                                 never changes a result, only the cost of a miss-heavy step */
+                                 and enough heads); 1: one-pass scan.  Both take the argmin of an fp32
+                                 sum of squares, associated differently: only a near-tie below
+                                 fp32 resolution can resolve differently (pin the mode for
+                                 bitwise reproducible decisions) */
   int32_t* feedback;          /* optional int32[2] (e.g. a pinned host buffer's device alias):
                                  {heads that missed, heads} over the steps since the last
                                  publication, stored at the start of every 8th step (the complete
@@ -248,6 +253,14 @@ typedef struct MacMatchRowsParams {
   int32_t* out_scanned;
 } MacMatchRowsParams;
 
+/* mac_build_ring: positions seq_lens[b] - n_rows + 1 .. seq_lens[b] of every request, whose K/V
+ * is already in the paged cache; q_pre is [B, n_rows, Hq, d] (their pre-RoPE queries, in_dtype). */
+typedef struct MacRingBuildParams {
+  int32_t n_rows;     /* 1 .. min(window, seq_lens[b]) */
+  int32_t n_chunks;   /* key splits per row block (>= 1); > 1 needs `part` */
+  void* part;         /* [B, n_rows, Hq, n_chunks, d_v + 1] f32 scratch (NULL when n_chunks == 1) */
+} MacRingBuildParams;
+
 int mac_abi_version(void);
 size_t mac_params_size(void);
 const char* mac_error_string(int code);
@@ -322,6 +335,11 @@ int mac_remove_summaries(int32_t n_rows, int32_t head_dim_v, const double* a_acc
 int mac_rope_rotate(int32_t n_rows, int32_t head_dim, const double* x, const double* t, const double* rope_freqs,
                     double* out, void* stream);
 int mac_match_rows(const MacMatchRowsParams* p, void* stream);
+/* Ring entries (ring_q, ring_qp, ring_acc, ring_lse) of the last rb->n_rows positions of every
+ * request from the cached KV: slot (t-1) % W <- (q_t, AS[1, t-r] under R_t q_t).  bf16 d = 128
+ * storage with 8 % (Hq / Hkv) == 0, page_size % 16 == 0, unsharded (else MAC_ERR_SHAPE: callers
+ * then run forced-miss decode steps).  Tensor-core pass; no seq_lens change. */
+int mac_build_ring(const MacDecodeParams* p, const MacRingBuildParams* rb, void* stream);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 9
+ABI_VERSION = 10
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -51,6 +51,7 @@ EXPORTS = (
     "mac_remove_summaries",
     "mac_rope_rotate",
     "mac_match_rows",
+    "mac_build_ring",
 )
 
 # per-head / per-group statistics fields of mac_step_stats (include/macattn.h)
@@ -191,6 +192,10 @@ class MacMatchRowsParams(C.Structure):
     ]
 
 
+class MacRingBuildParams(C.Structure):
+    _fields_ = [("n_rows", C.c_int32), ("n_chunks", C.c_int32), ("part", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -245,6 +250,8 @@ def load() -> C.CDLL:
     lib.mac_remove_summaries.argtypes = [C.c_int32, C.c_int32] + [C.c_void_p] * 4 + [C.c_double] + [C.c_void_p] * 4
     lib.mac_rope_rotate.restype = C.c_int
     lib.mac_rope_rotate.argtypes = [C.c_int32, C.c_int32] + [C.c_void_p] * 5
+    lib.mac_build_ring.restype = C.c_int
+    lib.mac_build_ring.argtypes = [C.POINTER(MacDecodeParams), C.POINTER(MacRingBuildParams), C.c_void_p]
     if lib.mac_abi_version() != ABI_VERSION:
         raise RuntimeError(f"libmacattn ABI {lib.mac_abi_version()} != expected {ABI_VERSION}; rebuild")
     if lib.mac_params_size() != C.sizeof(MacDecodeParams):

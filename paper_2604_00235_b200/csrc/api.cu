@@ -18,6 +18,8 @@ bool match_fast_supported(const MacDecodeParams&);
 bool front_fast_supported(const MacDecodeParams&);
 cudaError_t launch_merge_partials(const MacMergeParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_prefill_kv(const MacDecodeParams&, int, cudaStream_t);
+bool ring_build_supported(const MacDecodeParams&);
+cudaError_t launch_ring_build(const MacDecodeParams&, const MacRingBuildParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_step_stats(const MacDecodeParams&, double*, double*, cudaStream_t);
 template <int MODE> cudaError_t launch_mass_bound(const MacDecodeParams&, const MacMassBoundParams&, cudaStream_t);
 }  // namespace mac
@@ -199,6 +201,17 @@ int mac_prefill_kv(const MacDecodeParams* p, int32_t n_tokens, void* stream) {
     case MAC_MODE_BF16: return (int)launch_prefill_kv<MAC_MODE_BF16>(*p, n_tokens, st);
     default: return (int)launch_prefill_kv<MAC_MODE_F64>(*p, n_tokens, st);
   }
+}
+
+int mac_build_ring(const MacDecodeParams* p, const MacRingBuildParams* rb, void* stream) {
+  const int v = validate(p, true);
+  if (v) return v;
+  if (!rb) return MAC_ERR_NULL;
+  if (!ring_build_supported(*p)) return MAC_ERR_SHAPE;
+  if (rb->n_rows < 0 || rb->n_rows > p->window || rb->n_chunks < 1) return MAC_ERR_SHAPE;
+  if (rb->n_chunks > 1 && !rb->part) return MAC_ERR_NULL;
+  if (rb->n_rows == 0) return MAC_OK;
+  return (int)launch_ring_build(*p, *rb, static_cast<cudaStream_t>(stream));
 }
 
 int mac_step_stats(const MacDecodeParams* p, double* head_stats, double* group_stats, void* stream) {

@@ -141,7 +141,7 @@ class BatchDecodeEngine:
     def __init__(self, cfg: EngineConfig, batch: int, max_seq_len: int, *, device="cuda",
                  max_chunks: int | None = None, min_chunk: int = 128, page_perm_seed: int | None = None,
                  record_cached: bool = False, kv_offset: int = 0, kv_limit: int = 0, n_shards: int = 0,
-                 track_stats: bool = False):
+                 track_stats: bool = False, allocate_kv: bool = True):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         if max_seq_len < 1:
@@ -174,7 +174,17 @@ class BatchDecodeEngine:
         self.k_cache: list[torch.Tensor] = []
         self.v_cache: list[torch.Tensor] = []
         self.page_table = None
-        self._alloc_kv(max_seq_len)
+        # allocate_kv=False: the KV pool and block table are the caller's (attach_kv); the engine
+        # then owns only the rings, the per-layer positions and the workspace
+        self.external_kv = not allocate_kv
+        if allocate_kv:
+            self._alloc_kv(max_seq_len)
+        else:  # placeholders until attach_kv (never read: capacity 0 refuses every step)
+            self.page_table = torch.zeros(batch, 1, dtype=torch.int32, device=self.device)
+            self.k_cache = [torch.zeros(1, cfg.n_kv_heads, self.page_size, cfg.d, dtype=self.sdt, device=self.device)
+                            for _ in range(cfg.n_layers)]
+            self.v_cache = [torch.zeros(1, cfg.n_kv_heads, self.page_size, cfg.d_v, dtype=self.sdt,
+                                        device=self.device) for _ in range(cfg.n_layers)]
         B, Hq, W, d, dv = batch, cfg.n_q_heads, cfg.window, cfg.d, cfg.d_v
         L = cfg.n_layers
         self.ring_q = [torch.zeros(B, Hq, W, d, dtype=self.sdt, device=dev) for _ in range(L)]
@@ -200,8 +210,12 @@ class BatchDecodeEngine:
         # the last publication into this pinned buffer through its device alias; the engine
         # reads it WITHOUT a synchronisation (so it may be ~8-16 steps old) and takes the
         # one-pass scan unless misses are rare (< 1% of heads) — the two-pass match is built for
-        # the hit path.  Both scans are exact, so a stale choice only costs time.  match_mode="two_pass" /
-        # "one_pass" pin it (tests, profiling); "adaptive" is the default.
+        # the hit path.  Both scans take the argmin of an fp32 sum of squares but
+        # associate it differently (one-pass: 8-dim lane chunks + xor tree; two-pass: 16 planar
+        # dims + the other 112), so a near-tie below fp32 resolution (|Δd| ~ 1e-6 relative) may
+        # resolve differently between them — inside SURVEY §8c's documented near-tie band, never
+        # elsewhere.  match_mode="two_pass" / "one_pass" pin the scan for bitwise reproducible
+        # decisions; "adaptive" (the default) trades that for speed on miss-heavy steps.
         self.match_mode = "adaptive"
         self._fb_host = self._fb_alias = None
         if dev.type == "cuda":
@@ -253,8 +267,51 @@ class BatchDecodeEngine:
         self.__dict__.pop("_pcache", None)  # cached launch params hold the old pointers
         self.capacity = pps * ps
 
+    def attach_kv(self, k_cache, v_cache, block_table: torch.Tensor, seq_lens: torch.Tensor | None = None):
+        """Serve from a caller-owned paged KV pool — the serving-engine contract (vLLM / SGLang
+        block tables; the reference reads pages at kvstore.py:121-165).
+
+        k_cache / v_cache: one tensor per layer (a list, or a [n_layers, ...] tensor), each
+        [num_blocks, Hkv, page_size, d] (HND) in the storage dtype, post-RoPE keys as the append
+        writes them.  block_table: [B, max_blocks] int32 on the device; row b lists batch slot
+        b's blocks in token order (token t in block (t-1) // page_size).  Rows may share blocks
+        (a common prompt prefix) and may be permuted or edited in place between steps — the
+        kernels read the table every step; a decode step appends into the block holding its
+        position, so that block must belong to the request alone.  seq_lens: [B] tokens already
+        in the pool (default 0), applied to every layer.
+
+        The engine keeps its rings and per-layer positions; it never allocates or grows KV again
+        (reserve() raises once a request would pass max_blocks * page_size)."""
+        cfg, L = self.cfg, self.cfg.n_layers
+        ks = list(k_cache.unbind(0)) if isinstance(k_cache, torch.Tensor) else list(k_cache)
+        vs = list(v_cache.unbind(0)) if isinstance(v_cache, torch.Tensor) else list(v_cache)
+        if len(ks) != L or len(vs) != L:
+            raise ValueError(f"expected {L} per-layer K and V caches, got {len(ks)} and {len(vs)}")
+        nb = ks[0].shape[0]
+        for t, dv in [(k, cfg.d) for k in ks] + [(v, cfg.d_v) for v in vs]:
+            if (t.dim() != 4 or tuple(t.shape[1:]) != (cfg.n_kv_heads, self.page_size, dv) or t.shape[0] != nb
+                    or t.dtype != self.sdt or t.device != self.device or not t.is_contiguous()):
+                raise ValueError(f"KV cache must be contiguous [num_blocks, {cfg.n_kv_heads}, {self.page_size}, "
+                                 f"d] {self.sdt} on {self.device}; got {tuple(t.shape)} {t.dtype} {t.device}")
+        bt = block_table
+        if (bt.dim() != 2 or bt.shape[0] != self.batch or bt.dtype != torch.int32 or bt.device != self.device
+                or not bt.is_contiguous()):
+            raise ValueError(f"block_table must be a contiguous [{self.batch}, max_blocks] int32 tensor on "
+                             f"{self.device}")
+        self.k_cache, self.v_cache, self.page_table = ks, vs, bt
+        self.external_kv = True
+        self.capacity = bt.shape[1] * self.page_size
+        self.__dict__.pop("_pcache", None)
+        if seq_lens is not None:
+            for layer in range(L):
+                self.seq_lens[layer].copy_(seq_lens.to(self.device, torch.int32))
+                self._len[layer] = int(seq_lens.max().item())
+
     def reserve(self, tokens: int):
         """Grow the paged KV pool so every request can hold `tokens` tokens (doubling)."""
+        if tokens > self.capacity and self.external_kv:
+            raise ValueError(f"position {tokens} exceeds the caller-owned block table ({self.capacity} tokens per "
+                             f"request): extend block_table and attach_kv again")
         if tokens > self.capacity:
             self._alloc_kv(max(tokens, 2 * self.capacity))
 
@@ -473,12 +530,20 @@ class BatchDecodeEngine:
         _lib.check(_lib.load().mac_mass_bound(P, mb, self._stream()), "mac_mass_bound")
         return out
 
-    def prefill(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor) -> BatchStepResult | None:
+    def prefill(self, layer: int, q_pre: torch.Tensor, k_pre: torch.Tensor, v: torch.Tensor,
+                *, ring_build: str = "auto") -> BatchStepResult | None:
         """Append a prompt of n tokens to every request ([B, n, H, d] tensors, token-major) and
-        leave the ring exactly as n forced-miss decode steps would: the first
-        n - min(n, W) tokens go through one bulk append (mac_prefill_kv), the last min(n, W)
-        through decode steps that all take the miss path, so every ring slot holds the exact
-        prefix summary AS[1, t-r] under q_t.  Returns the last step's result."""
+        leave exactly the state of n forced-miss decode steps: KV of
+        positions 1..n and ring slots holding (q_t, AS[1, t-r] under q_t) for the last min(n, W)
+        positions.  Returns the last token's step result (its output is exact attention over
+        [1, n]).
+
+        GEMM form (ring_build="auto" on the bf16 d = 128 path, or "gemm"): tokens 1..n-1 in one
+        bulk append (mac_prefill_kv), the ring entries of positions n-c..n-1 (c = min(W, n) - 1)
+        in one tensor-core pass over the cache (mac_build_ring: every key tile read once per
+        block of query rows), then token n as one forced-miss decode step.  ring_build="steps"
+        (and every other storage / shape) runs the last min(n, W) tokens as forced-miss decode
+        steps instead."""
         self._layer(layer)
         cfg, B = self.cfg, self.batch
         if q_pre.dim() != 4 or q_pre.shape[0] != B or q_pre.shape[2:] != (cfg.n_q_heads, cfg.d):
@@ -486,12 +551,19 @@ class BatchDecodeEngine:
         n = q_pre.shape[1]
         if tuple(k_pre.shape) != (B, n, cfg.n_kv_heads, cfg.d) or tuple(v.shape) != (B, n, cfg.n_kv_heads, cfg.d_v):
             raise ValueError("key/value shapes do not match [B, n, Hkv, d]")
+        if ring_build not in ("auto", "gemm", "steps"):
+            raise ValueError(f"ring_build must be 'auto', 'gemm' or 'steps', got {ring_build!r}")
         if n == 0:
             return None
         stored = int(self.seq_lens[layer].max().item()) if self.capacity else 0
         self._len[layer] = max(self._len[layer], stored)
         self._ensure_room(layer, n + 1)
-        n_bulk = n - min(n, cfg.window)
+        gemm = ring_build != "steps" and self.ring_build_supported()
+        if ring_build == "gemm" and not gemm:
+            raise ValueError("the GEMM-form ring build needs bf16 storage, d = d_v = 128, 8 % (Hq/Hkv) == 0, "
+                             "page_size % 16 == 0 and an unsharded cache")
+        n_steps = 1 if gemm else min(n, cfg.window)
+        n_bulk = n - n_steps
         if n_bulk:
             kb, vb = k_pre[:, :n_bulk].contiguous(), v[:, :n_bulk].contiguous()
             dt = _IN_DT[kb.dtype]
@@ -500,6 +572,10 @@ class BatchDecodeEngine:
             code = _lib.load().mac_prefill_kv(P, n_bulk, self._stream())
             _lib.check(code, "mac_prefill_kv")
             self._len[layer] += n_bulk
+        if gemm:
+            rows = min(cfg.window, n) - 1
+            if rows > 0:
+                self.build_ring(layer, q_pre[:, n_bulk - rows:n_bulk])
         res = None
         self._in_prefill = True  # prompt tokens are not decode decisions: no statistics
         try:
@@ -509,6 +585,45 @@ class BatchDecodeEngine:
         finally:
             self._in_prefill = False
         return res
+
+    def ring_build_supported(self) -> bool:
+        cfg = self.cfg
+        g = cfg.n_q_heads // cfg.n_kv_heads
+        return (cfg.storage == "bf16" and cfg.d == 128 and cfg.d_v == 128 and 8 % g == 0
+                and self.page_size % 16 == 0 and self.kv_offset == 0 and self.kv_limit == 0)
+
+    def build_ring(self, layer: int, q_rows: torch.Tensor, n_chunks: int | None = None):
+        """Ring entries of the last q_rows.shape[1] stored positions of every request from the KV
+        already in the cache (mac_build_ring): slot (t-1) % W <- (q_t, AS[1, t-r] under R_t q_t).
+        q_rows: [B, n_rows, Hq, d] pre-RoPE queries of positions seq_len-n_rows+1 .. seq_len (a
+        caller-owned pool filled by the serving system's own prefill works the same way).
+        n_chunks splits each row block's keys for parallelism (default: enough CTAs for ~4
+        waves on 148 SMs)."""
+        cfg, B = self.cfg, self.batch
+        if not self.ring_build_supported():
+            raise ValueError("mac_build_ring needs the bf16 d = 128 path (see prefill)")
+        if q_rows.dim() != 4 or q_rows.shape[0] != B or q_rows.shape[2:] != (cfg.n_q_heads, cfg.d):
+            raise ValueError(f"expected queries [B={B}, n_rows, {cfg.n_q_heads}, {cfg.d}]")
+        n_rows = q_rows.shape[1]
+        if n_rows > cfg.window:
+            raise ValueError(f"{n_rows} rows exceed the ring window {cfg.window}")
+        if n_rows == 0:
+            return
+        q_rows = q_rows.contiguous()
+        g = cfg.n_q_heads // cfg.n_kv_heads
+        blocks = B * cfg.n_kv_heads * -(-n_rows // (8 * (8 // g)))
+        if n_chunks is None:
+            longest = int(self.seq_lens[layer].max().item())
+            n_chunks = max(1, min(-(-4 * SM_COUNT_B200 // blocks), -(-longest // 2048)))
+        part = None
+        if n_chunks > 1:
+            part = torch.empty(B * n_rows * cfg.n_q_heads * n_chunks * (cfg.d_v + 1), dtype=torch.float32,
+                               device=self.device)
+        P = self._build_params(layer, q_rows, q_rows, q_rows, _IN_DT[q_rows.dtype], False)
+        rb = _lib.MacRingBuildParams(n_rows=n_rows, n_chunks=n_chunks, part=part.data_ptr() if part is not None else None)
+        # (part is freed back to the caching allocator on this stream: stream order keeps it live
+        # until the merge kernel has read it)
+        _lib.check(_lib.load().mac_build_ring(C.byref(P), C.byref(rb), C.c_void_p(self._stream())), "mac_build_ring")
 
     def match_path(self, P=None) -> int:
         """mac_match_path of a parameter set (default: the last step's): which scan, verify layout

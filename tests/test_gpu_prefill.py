@@ -86,3 +86,64 @@ def test_prefill_rejects_bad_shapes():
     z = torch.zeros(1, 4, 8, 128, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError):
         eng.prefill(0, z, z, z)  # keys must have Hkv = 2 heads
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_build_ring_gemm_form_matches_decode_steps(chunks):
+    """The tensor-core ring build (mac_build_ring) against the forced-miss decode steps it
+    replaces, on the same prompt: ring queries identical, summaries within 2e-5, with one key
+    chunk and with split keys (merge kernel).  GQA 32/8 and 8/1 (g = 4, 8), a band and r = 0."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    for hq, hkv, n, W, r in ((32, 8, 700, 128, 32), (8, 1, 333, 64, 0)):
+        B = 2
+        trs = [gen_synthetic(SyntheticSpec(seq_len=n, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=90 + s))
+               for s in range(B)]
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)  # noqa: E731
+        q = dev(np.stack([t.q_pre[:, 0] for t in trs]))
+        k = dev(np.stack([t.k_pre[:, 0] for t in trs]))
+        v = dev(np.stack([t.v[:, 0] for t in trs]))
+        cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+        a = BatchDecodeEngine(cfg, B, n + 8, page_perm_seed=2, min_chunk=32)
+        s = BatchDecodeEngine(cfg, B, n + 8, page_perm_seed=3, min_chunk=32)
+        s.prefill(0, q, k, v, ring_build="steps")
+        # GEMM form on its own: bulk append n tokens, then build every ring slot (no final step)
+        P = a._build_params(0, q[:, 0].contiguous(), k.contiguous(), v.contiguous(), 1, False)
+        from paper_2604_00235_b200 import _lib
+
+        _lib.check(_lib.load().mac_prefill_kv(P, n, a._stream()), "mac_prefill_kv")
+        a._len[0] = n
+        a.build_ring(0, q[:, n - W:], n_chunks=chunks)
+        torch.cuda.synchronize()
+        assert torch.equal(a.ring_q[0], s.ring_q[0])
+        assert torch.equal(a.ring_qp[0], s.ring_qp[0])
+        la, ls = a.ring_lse[0].double(), s.ring_lse[0].double()
+        fin = torch.isfinite(ls)
+        assert torch.equal(torch.isfinite(la), fin)
+        assert (la[fin] - ls[fin]).abs().max().item() <= 2e-5
+        ra, rs = a.ring_acc[0].double(), s.ring_acc[0].double()
+        rel = (ra - rs).norm(dim=-1) / rs.norm(dim=-1).clamp_min(1e-30)
+        assert rel[fin].max().item() <= 2e-5, rel[fin].max().item()
+
+
+def test_prefill_gemm_and_steps_agree_on_the_next_decode():
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
+
+    B, hq, hkv, n, W, r = 2, 8, 2, 400, 64, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=n + 20, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=95 + s))
+           for s in range(B)]
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)  # noqa: E731
+    q = dev(np.stack([t.q_pre[:, 0] for t in trs]))
+    k = dev(np.stack([t.k_pre[:, 0] for t in trs]))
+    v = dev(np.stack([t.v[:, 0] for t in trs]))
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    a = BatchDecodeEngine(cfg, B, n + 32, min_chunk=32)
+    s = BatchDecodeEngine(cfg, B, n + 32, min_chunk=32)
+    ra = a.prefill(0, q[:, :n], k[:, :n], v[:, :n], ring_build="gemm").out.clone()
+    rs = s.prefill(0, q[:, :n], k[:, :n], v[:, :n], ring_build="steps").out.clone()
+    assert ((ra - rs).norm(dim=-1) / rs.norm(dim=-1)).max().item() <= 1e-5
+    for m in range(n, n + 20):
+        x = a.decode_step(0, q[:, m].contiguous(), k[:, m].contiguous(), v[:, m].contiguous())
+        y = s.decode_step(0, q[:, m].contiguous(), k[:, m].contiguous(), v[:, m].contiguous())
+        assert torch.equal(x.match_hit, y.match_hit) and torch.equal(x.match_pos, y.match_pos)
+        assert ((x.out - y.out).norm(dim=-1) / y.out.norm(dim=-1)).max().item() <= 1e-4
