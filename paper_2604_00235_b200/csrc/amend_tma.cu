@@ -24,6 +24,8 @@
 // Split band (common.cuh band_items): the producer first streams the CTA's static band items,
 // which need only what the front kernel wrote, then waits on the grid dependency (the verify
 // kernel's plan) and claims piece items from the device work list one at a time.
+// Development variant (MAC_DEV_KNOBS builds only, MAC_AMEND_TMA=1): see amend_mma.cu hit_amend_tma.
+#ifdef MAC_DEV_KNOBS
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdio.h>
@@ -434,3 +436,4 @@ cudaError_t launch_amend_tma(const MacDecodeParams& p, cudaStream_t st, int nb) 
 }
 
 }  // namespace mac
+#endif  // MAC_DEV_KNOBS

@@ -150,6 +150,8 @@ class BatchDecodeEngine:
         self.cfg = cfg
         self.batch = batch
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None and torch.cuda.is_available():
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.sdt = _TORCH_STORAGE[cfg.storage]
         self.sumdt = torch.float64 if cfg.storage == "f64" else torch.float32
         self.group = cfg.n_q_heads // cfg.n_kv_heads

@@ -42,7 +42,7 @@ def _stream(dev: torch.device) -> int:
 
 
 def _f64(x, dev) -> torch.Tensor:
-    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    return torch.from_numpy(np.array(x, dtype=np.float64, order="C")).to(dev)  # a writable host copy
 
 
 def _ptr(t) -> int | None:
