@@ -17,14 +17,9 @@ namespace mac {
 __device__ unsigned long long g_amend_trace[4096 * 8];
 #endif
 
-#ifdef MAC_DEV_KNOBS
 bool amend_tma_supported(const MacDecodeParams& p);
 int amend_tma_grid(cudaError_t* err);
 cudaError_t launch_amend_tma(const MacDecodeParams& p, cudaStream_t st, int nb);
-#else  // the TMA amend is compiled into development builds only
-static int amend_tma_grid(cudaError_t*) { return 1; }
-static cudaError_t launch_amend_tma(const MacDecodeParams&, cudaStream_t, int) { return cudaErrorNotSupported; }
-#endif
 
 bool amend_mma_supported(const MacDecodeParams& p) {
   const int g = p.n_q_heads / p.n_kv_heads;
@@ -167,22 +162,25 @@ static int amend_grid_full(int vi, cudaError_t* err) {
 // one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
 // (1..4).  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
 // kernel's plan and this launch call it with the same parameters, so they always agree.
-// The TMA amend (amend_tma.cu) is a development variant: on B200 it measured slower than the
-// one-warp kernel on the C3 step (amend 34.3 vs 27 us) and hung or faulted intermittently on a
-// one-pass 32K step with misses (profiles/r02/SUMMARY.md), so the product library never launches
-// it; development builds select it with MAC_AMEND_TMA=1.
+// Which kernel runs the hit step's amend.  With fewer GQA groups than SMs (C2: B = 8, 8 KV heads)
+// each group's items are long and few, and the one-warp kernel streams an item at ~5 GB/s per
+// warp (its 2-stage lookahead covers one DRAM round trip per 32 tokens), so the TMA kernel
+// (amend_tma.cu: a producer warp keeps three 32-token stages in flight per CTA, three consumer
+// warps share each item) ends the C2 amend 6 us earlier; with many groups (C3: 256) the one-warp
+// kernel's 6-7 independent warps per SM win (in-step timelines, profiles/r02/SUMMARY.md).
+// Development builds can force either with MAC_AMEND_TMA=0 / 1 (3 consumers, 3 stages) / 2
+// (6 consumers, 6 stages).
 static bool hit_amend_tma(const MacDecodeParams& p) {
+  bool want = p.batch * p.n_kv_heads < 148;
 #ifdef MAC_DEV_KNOBS
   static int forced = -2;
   if (forced == -2) {
     const char* env = getenv("MAC_AMEND_TMA");
-    forced = env ? atoi(env) : 0;
+    forced = env ? atoi(env) : -1;
   }
-  return forced == 1 && p.n_shards == 0 && amend_tma_supported(p);
-#else
-  (void)p;
-  return false;
+  if (forced >= 0) want = forced >= 1;
 #endif
+  return want && p.n_shards == 0 && amend_tma_supported(p);
 }
 
 int band_split(const MacDecodeParams& p) {

@@ -24,28 +24,33 @@
 // Split band (common.cuh band_items): the producer first streams the CTA's static band items,
 // which need only what the front kernel wrote, then waits on the grid dependency (the verify
 // kernel's plan) and claims piece items from the device work list one at a time.
-// Development variant (MAC_DEV_KNOBS builds only, MAC_AMEND_TMA=1): see amend_mma.cu hit_amend_tma.
-#ifdef MAC_DEV_KNOBS
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "amend_mma.cuh"
 
 namespace mac {
 
 namespace {
-constexpr int TA_NC = 3;                      // consumer warps per CTA
-constexpr int TA_THREADS = 32 * (TA_NC + 1);  // + one producer warp
-constexpr int TA_NS = 5;                      // 32-token stages in the ring
 constexpr int TA_STAGE = 4 * TILE_BYTES;      // K sub-tiles 0, 1 then V sub-tiles 0, 1
 constexpr int TA_ND = 4;                      // item descriptor slots
 constexpr int TA_PART = 8 * 2 * 129;          // one consumer's partials: [head][set][acc..., lse]
-constexpr int OFF_SCRATCH = TA_NS * TA_STAGE;
-constexpr int OFF_DESC = OFF_SCRATCH + TA_NC * TA_PART * 4;
-constexpr int OFF_BAR = OFF_DESC + TA_ND * 32;
-constexpr int TA_SMEM_USED = OFF_BAR + 8 * (2 * TA_NS + 2 * TA_ND);
-constexpr int TA_SMEM = TA_SMEM_USED + 1024;  // the ring needs a 1024-byte aligned base
+// Ring geometry per variant: NC consumer warps, NS 32-token stages.  NS must be a multiple of NC:
+// consumers take an item's stages round-robin, so a stage slot is then always refilled for the
+// consumer that drained it, which is what keeps every waiter within one phase of the slot's
+// full barrier (a parity wait cannot tell phase L from L-2: with NS = 5, NC = 3 a consumer could
+// pass the wait for lap L while lap L-1's TMA was still landing — the intermittent hang/fault
+// measured in round 2).
+template <int NC, int NS> struct TmaRing {
+  static_assert(NS % NC == 0, "NS must be a multiple of NC");
+  static constexpr int THREADS = 32 * (NC + 1);  // + one producer warp
+  static constexpr int OFF_SCRATCH = NS * TA_STAGE;
+  static constexpr int OFF_DESC = OFF_SCRATCH + NC * TA_PART * 4;
+  static constexpr int OFF_BAR = OFF_DESC + TA_ND * 32;
+  static constexpr int SMEM = OFF_BAR + 8 * (2 * NS + 2 * TA_ND) + 1024;  // + 1024-byte alignment
+};
 
 __device__ __forceinline__ void mbar_init(uint32_t a, unsigned n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
@@ -75,14 +80,17 @@ __device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void consumers_sync() {  // the TA_NC consumer warps only (named barrier 1)
-  asm volatile("bar.sync 1, %0;" ::"n"(TA_NC * 32) : "memory");
+template <int NC> __device__ __forceinline__ void consumers_sync() {  // the NC consumer warps (named barrier 1)
+  asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
 }
 }  // namespace
 
-__global__ void __launch_bounds__(TA_THREADS, 2)
+template <int TA_NC, int TA_NS, int MINB>
+__global__ void __launch_bounds__(TmaRing<TA_NC, TA_NS>::THREADS, MINB)
     amend_tma_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                      MacDecodeParams p, int nb) {
+  using R = TmaRing<TA_NC, TA_NS>;
+  constexpr int OFF_SCRATCH = R::OFF_SCRATCH, OFF_DESC = R::OFF_DESC, OFF_BAR = R::OFF_BAR;
   extern __shared__ unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       S.reset();
     }
     write_partial(S, scr, 1, row, q4, g);
-    consumers_sync();
+    consumers_sync<TA_NC>();
     // merge the TA_NC consumers' partials of each (head, set) and store the item's slot
     float* out = part + ((int64_t)(grp * p.max_chunks + c) * g) * 2 * 129;
     for (int hs = cw; hs < 2 * g; hs += TA_NC) {
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       }
       if (lane == 0) out[hs * 129 + 128] = Z > 0.f ? L + __logf(Z) : -CUDART_INF_F;
     }
-    consumers_sync();  // scratch free for the next item
+    consumers_sync<TA_NC>();  // scratch free for the next item
     if (lane == 0) mbar_arrive(bar_dempty + 8 * ds);
   }
   if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -386,11 +394,36 @@ static bool encode_cache_map(CUtensorMap* m, const void* ptr) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// CTAs of the persistent grid (2 per SM); sets the shared-memory attribute on first use
+// variants (MAC_AMEND_TMA = 1, 2): (consumers, stages, CTAs per SM)
+struct TmaVariant {
+  void (*fn)(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, MacDecodeParams, int);
+  int threads, smem;
+};
+static const TmaVariant kTma[] = {
+    {amend_tma_kernel<3, 3, 2>, TmaRing<3, 3>::THREADS, TmaRing<3, 3>::SMEM},
+#ifdef MAC_DEV_KNOBS
+    {amend_tma_kernel<6, 6, 1>, TmaRing<6, 6>::THREADS, TmaRing<6, 6>::SMEM},
+#endif
+};
+static int tma_variant() {
+#ifdef MAC_DEV_KNOBS
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("MAC_AMEND_TMA");
+    v = (env && atoi(env) == 2) ? 1 : 0;
+  }
+  return v;
+#else
+  return 0;
+#endif
+}
+
+// CTAs of the persistent grid (occupancy x SMs); sets the shared-memory attribute on first use
 int amend_tma_grid(cudaError_t* err) {
   static int grid = 0;
   if (!grid) {
-    cudaError_t e = cudaFuncSetAttribute(amend_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM);
+    const TmaVariant& tv = kTma[tma_variant()];
+    cudaError_t e = cudaFuncSetAttribute(tv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tv.smem);
     if (e != cudaSuccess) {
       if (err) *err = e;
       return 0;
@@ -398,7 +431,7 @@ int amend_tma_grid(cudaError_t* err) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amend_tma_kernel, TA_THREADS, TA_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tv.fn, tv.threads, tv.smem);
     grid = sms * (per_sm < 1 ? 1 : per_sm);
   }
   return grid;
@@ -424,16 +457,16 @@ cudaError_t launch_amend_tma(const MacDecodeParams& p, cudaStream_t st, int nb) 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(gfull);
-  cfg.blockDim = dim3(TA_THREADS);
-  cfg.dynamicSmemBytes = TA_SMEM;
+  const TmaVariant& tv = kTma[tma_variant()];
+  cfg.blockDim = dim3(tv.threads);
+  cfg.dynamicSmemBytes = tv.smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, amend_tma_kernel, mK, mV, p, nb);
+  return cudaLaunchKernelEx(&cfg, tv.fn, mK, mV, p, nb);
 }
 
 }  // namespace mac
-#endif  // MAC_DEV_KNOBS

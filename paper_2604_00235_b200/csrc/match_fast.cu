@@ -264,19 +264,28 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 //      planned by its CTA (or by its last-decided head with PER_HEAD).
 // rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
 template <bool PER_HEAD, int kQDims>
-__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget) {
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget, int append) {
   constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
   constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
   constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
   constexpr int G = 32 / LR;                       // rows per warp-round
   TL_MARK(p, TL_VERIFY_IN);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  TL_MARK(p, TL_VERIFY_WAITED);
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
   const int grp = PER_HEAD ? blockIdx.x / g : blockIdx.x;
   const int hl = PER_HEAD ? blockIdx.x % g : warp;
+  // The step's KV append + query rotation (one warp per (request, kv head)) runs here, before the
+  // wait for the scan: it does not depend on the scan, and in the scan kernel its chain of
+  // dependent loads ended the front grid ~4.5 us after the last scan CTA at C2 (r02 timeline).
+  // The amend's band items read what it writes before their own wait, so it is fenced before this
+  // CTA's launch_dependents (the amend grid starts only after every verify CTA triggered).
+  if (append && hl == 0) {
+    append_warp(p, grp, 0, 0);
+    __threadfence();
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL_MARK(p, TL_VERIFY_WAITED);
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int b = grp / Hkv, kvh = grp % Hkv;
   const int bh = b * Hq + kvh * g + hl;
   const int nsum = ((W + rows - 1) / rows) * (kThreads / 32);  // scan warps of this head
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   TL_MARK(p, TL_VERIFY_OUT);
 }
 
-cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims) {
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims, int append) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads);
   cfg.blockDim = dim3(per_head ? 32 : 32 * (p.n_q_heads / p.n_kv_heads));
@@ -477,13 +486,13 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
   const int nt = nb > 0 ? piece_target(p) : 0;
   if (qdims == 16)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, append)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, append);
   if (qdims == 32)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt);
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, append)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, append);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, append)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, append);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -558,16 +567,20 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const bool per_head = !per_group && p.batch * p.n_q_heads >= 148;
   const bool two_pass = do_match && front_two_pass(p);
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
+  // a whole two-pass step: the append rides in the verify kernel's prologue (verify_kernel)
+  const bool app_in_verify = two_pass && do_append && passes == 3 && !rotate_only && !plan;
+  const bool app_in_front = do_append && !app_in_verify;
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
-  const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
-  if (n_match + n_append == 0) return cudaSuccess;
+  const int n_append = app_in_front ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
+  if (n_match + n_append + (app_in_verify ? 1 : 0) == 0) return cudaSuccess;
   if (passes & 1) {
     auto fn = (do_match && u.fn_planar && p.ring_qp) ? u.fn_planar : u.fn;
-    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
+    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, app_in_front ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
-  if ((passes & 2) && u.two_pass && do_match) return launch_verify(p, st, per_head, u.rows, u.qdims);
+  if ((passes & 2) && u.two_pass && do_match)
+    return launch_verify(p, st, per_head, u.rows, u.qdims, app_in_verify ? 1 : 0);
   return cudaSuccess;
 }
 

@@ -374,7 +374,7 @@ def test_run_decode_oracle_modes_and_traffic_identity():
     for eng in (a, b):
         assert eng.traffic.tokens_read == eng.metrics.kv_tokens_read
         assert eng.metrics.hits > 0
-    assert compute_metrics(a.metrics)["acceptance"] == compute_metrics(b.metrics)["acceptance"]
+    assert compute_metrics(a.metrics)["acceptance_rate"] == compute_metrics(b.metrics)["acceptance_rate"]
 
 
 def test_rectify_append_validation_and_ring_write():
