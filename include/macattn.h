@@ -155,7 +155,9 @@ typedef struct MacDecodeParams {
   size_t workspace_bytes;
   /* ---- match-scan choice (bf16 d = 128 path) ------------------------------ */
   int32_t match_mode;         /* 0: by geometry (two-pass scan + verify for rings of 512..1024 rows
-                                 and enough heads); 1: one-pass scan.  Both take the argmin of an fp32
+                                 and enough heads); 1: one-pass scan; 2: two-pass with the full
+                                 walks of heads without a near-repeat spread over the GPU
+                                 (dense_kernel; per-group verify geometry, else as 0).  Both take the argmin of an fp32
                                  sum of squares, associated differently: only a near-tie below
                                  fp32 resolution can resolve differently (pin the mode for
                                  bitwise reproducible decisions) */
@@ -279,7 +281,9 @@ enum {
   MAC_PATH_TWO_PASS = 1,      /* two-pass match: planar scan + verify kernel */
   MAC_PATH_VERIFY_GROUP = 2,  /* verify: one CTA per GQA group */
   MAC_PATH_VERIFY_HEAD = 4,   /* verify: one CTA per head */
-  MAC_PATH_AMEND_MMA = 8      /* bf16 d = 128 tensor-core amend (else the generic CUDA-core amend) */
+  MAC_PATH_AMEND_MMA = 8,     /* bf16 d = 128 tensor-core amend (else the generic CUDA-core amend) */
+  MAC_PATH_DENSE_KERNEL = 16, /* match_mode 2: heads with no near-repeat are walked by dense_kernel */
+  MAC_PATH_AMEND_TMA = 32     /* the hit step's amend is the TMA-fed kernel (few GQA groups) */
 };
 int mac_match_path(const MacDecodeParams* p);
 

@@ -20,7 +20,7 @@ MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
 MATCH_PRE_ROPE, MATCH_POST_ROPE = 0, 1
 DOWNDATE_SPLIT, DOWNDATE_REMOVE = 0, 1
-PATH_TWO_PASS, PATH_VERIFY_GROUP, PATH_VERIFY_HEAD, PATH_AMEND_MMA = 1, 2, 4, 8
+PATH_TWO_PASS, PATH_VERIFY_GROUP, PATH_VERIFY_HEAD, PATH_AMEND_MMA, PATH_DENSE_KERNEL, PATH_AMEND_TMA = 1, 2, 4, 8, 16, 32
 
 EXPORTS = (
     "mac_abi_version",

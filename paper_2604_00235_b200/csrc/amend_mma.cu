@@ -183,6 +183,8 @@ static bool hit_amend_tma(const MacDecodeParams& p) {
   return want && p.n_shards == 0 && amend_tma_supported(p);
 }
 
+bool amend_uses_tma(const MacDecodeParams& p) { return hit_amend_tma(p); }
+
 int band_split(const MacDecodeParams& p) {
 #ifdef MAC_DEV_KNOBS
   static int forced = -2;

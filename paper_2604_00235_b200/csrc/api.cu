@@ -141,8 +141,12 @@ int mac_match_path(const MacDecodeParams* p) {
   if (p->storage == MAC_MODE_BF16 && match_fast_supported(*p) && front_two_pass(*p)) {
     path |= MAC_PATH_TWO_PASS;
     path |= verify_per_group(*p) ? MAC_PATH_VERIFY_GROUP : MAC_PATH_VERIFY_HEAD;
+    if (dense_deferred(*p)) path |= MAC_PATH_DENSE_KERNEL;
   }
-  if (p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) path |= MAC_PATH_AMEND_MMA;
+  if (p->storage == MAC_MODE_BF16 && amend_mma_supported(*p)) {
+    path |= MAC_PATH_AMEND_MMA;
+    if (amend_uses_tma(*p)) path |= MAC_PATH_AMEND_TMA;
+  }
   const int nb = (p->storage == MAC_MODE_BF16) ? band_split(*p) : 0;
   return path | (nb << 8);
 }

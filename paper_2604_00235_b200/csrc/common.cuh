@@ -266,7 +266,8 @@ struct Workspace {
                      //              4 heads missed and 6 steps completed since the feedback was last published
                      //              (complete adds; every 8th step's append warps publish and reset)
                      //              2 KV overflow flag (an append found no page for its token; sticky)
-                     //              (3, 5, 7-15 spare)
+                     //              8 dense heads deferred by the verify (match_mode 2; reset by complete)
+                     //              (3, 5, 7, 9-15 spare)
   size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  piece splits planned for the group | band items requested << 16
   size_t mpos_off;   // [B] i32      position m of this step
@@ -278,6 +279,9 @@ struct Workspace {
   size_t hpart_off;  // [B*Hq*W] f32  two-pass match: distance over the first d/2 dims per ring row
   size_t wsum_off;   // [B*Hq*kMaxWsum] uint4  two-pass match: per scan warp {P1, slot1, P2, slot2},
                      //                 its two smallest partials (fp32 bits) and their ring slots
+  size_t dstate_off; // [B*Hq] int4   two-pass match, dense heads deferred to dense_kernel (match_mode 2):
+                     //               {bound D* (fp32 bits), candidate slot 1, candidate slot 2, -}
+  size_t dlist_off;  // [B*Hq] i32    the deferred heads (bh), ctr[8] of them (reset by complete)
   size_t tl_off;     // [kTlSlots][2] u64 timeline stamps (MAC_TIMELINE builds only)
   size_t total;
 };
@@ -300,7 +304,9 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.part_off = align256(w.qrot_off + acc * rows * p.head_dim);
   w.hpart_off = align256(w.part_off + acc * rows * p.max_chunks * 2 * (p.head_dim_v + 1));
   w.wsum_off = align256(w.hpart_off + 4 * rows * (size_t)p.window);
-  w.tl_off = align256(w.wsum_off + 16 * rows * (size_t)kMaxWsum);
+  w.dstate_off = align256(w.wsum_off + 16 * rows * (size_t)kMaxWsum);
+  w.dlist_off = align256(w.dstate_off + 16 * rows);
+  w.tl_off = align256(w.dlist_off + 4 * rows);
 #ifdef MAC_TIMELINE
   w.total = align256(w.tl_off + 16 * kTlSlots);
 #else
@@ -405,6 +411,8 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
 bool match_fast_supported(const MacDecodeParams& p);
 bool front_two_pass(const MacDecodeParams& p);
 bool verify_per_group(const MacDecodeParams& p);
+bool dense_deferred(const MacDecodeParams& p);
+bool amend_uses_tma(const MacDecodeParams& p);
 bool amend_mma_supported(const MacDecodeParams& p);
 int band_split(const MacDecodeParams& p);
 int piece_target(const MacDecodeParams& p);

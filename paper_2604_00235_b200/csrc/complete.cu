@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(128) complete_kernel(MacDecodeParams p, int fu
     unsigned int* ctr = ws_ptr<unsigned int>(p, workspace_layout(p).ctr_off);
     ctr[0] = 0u;
     ctr[1] = 0u;
+    ctr[8] = 0u;
   }
 }
 
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
       unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
       ctr[0] = 0u;
       ctr[1] = 0u;
+      ctr[8] = 0u;
     }
   }
   if (live) {
@@ -89,6 +91,7 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
       unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
       ctr[0] = 0u;
       ctr[1] = 0u;
+      ctr[8] = 0u;
     }
     float Mp = NINF, Sp = 0.f, Mb = NINF, Sb = 0.f, ap[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
     for (int cb = 0; cb < nsl; cb += 8) {

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 //      planned by its CTA (or by its last-decided head with PER_HEAD).
 // rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
 template <bool PER_HEAD, int kQDims>
-__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget, int append) {
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget, int defer) {
   constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
   constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
   constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
@@ -274,15 +274,6 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
   const int grp = PER_HEAD ? blockIdx.x / g : blockIdx.x;
   const int hl = PER_HEAD ? blockIdx.x % g : warp;
-  // The step's KV append + query rotation (one warp per (request, kv head)) runs here, before the
-  // wait for the scan: it does not depend on the scan, and in the scan kernel its chain of
-  // dependent loads ended the front grid ~4.5 us after the last scan CTA at C2 (r02 timeline).
-  // The amend's band items read what it writes before their own wait, so it is fenced before this
-  // CTA's launch_dependents (the amend grid starts only after every verify CTA triggered).
-  if (append && hl == 0) {
-    append_warp(p, grp, 0, 0);
-    __threadfence();
-  }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL_MARK(p, TL_VERIFY_WAITED);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -369,7 +360,26 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   // verify CTAs' registers, which evicts the amend's band items from the SMs during the verify:
   // +2.3 us on the all-hit C3 step.)
   const int n_need = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(need));
-  if (2 * n_need >= nsum) {
+  bool deferred = false;
+  if (!PER_HEAD && defer && 2 * n_need >= nsum) {
+    // match_mode 2: hand the dense walk to dense_kernel, which spreads it over the whole GPU
+    // (a CTA per 128-row chunk); this head's candidates seed its key, and its group is planned
+    // by whichever dense chunk decides the group's last head
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other > key ? other : key;
+    }
+    if (lane == 0) {
+      const Workspace ws = workspace_layout(p);
+      if (key) atomicMax(ws_ptr<unsigned long long>(p, ws.mkey_off) + bh, key);
+      ws_ptr<int4>(p, ws.dstate_off)[bh] = make_int4((int)Dbits, cs1, cs2, 0);
+      const unsigned i = atomicAdd(ws_ptr<unsigned int>(p, ws.ctr_off) + 8, 1u);
+      ws_ptr<int>(p, ws.dlist_off)[i] = bh;
+    }
+    deferred = true;
+    need = 0u;
+  } else if (2 * n_need >= nsum) {
     constexpr int RK = 32 / G;  // rows per lane group per iteration
 #pragma unroll 1
     for (int base = 0; base < W; base += 32) {
@@ -462,18 +472,129 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     return;
   }
   __shared__ int slo[8];
-  if (lane == 0) slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
-  __syncthreads();
+  if (lane == 0 && !deferred) slo[hl] = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
+  const int n_def = __syncthreads_count(lane == 0 && deferred);
   TL_MARK(p, TL_V_DECIDED);
   if (threadIdx.x == 0) {  // (the amend reads the plan after this grid completes: no fence needed)
-    int lo_g = m;
-    for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
-    plan_group(p, b, kvh, m, lo_g, nb, ntarget);
+    if (n_def == 0) {
+      int lo_g = m;
+      for (int j = 0; j < g; ++j) lo_g = slo[j] < lo_g ? slo[j] : lo_g;
+      plan_group(p, b, kvh, m, lo_g, nb, ntarget);
+    } else {  // the decided heads count toward the group; dense_kernel's deciders plan it
+      __threadfence();
+      atom_add_acq_rel(ws_ptr<unsigned int>(p, workspace_layout(p).gcnt_off) + grp, (unsigned)(g - n_def));
+    }
   }
   TL_MARK(p, TL_VERIFY_OUT);
 }
 
-cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims, int append) {
+// match_mode 2, after the verify: the full distances of every ring row of the heads the verify
+// deferred (a query with no near-repeat makes every row survive pass 1), one warp per 128-row
+// chunk over the whole GPU instead of one warp walking 1024 rows — the same survivor test and the
+// same fp32 sums as the verify's walk (P(row) + the remaining 112 dims, reduced over 16 lanes), so
+// the argmin is the one the verify would have found.  Chunks publish their best key with an
+// atomic max; the chunk completing a head decides it (finish_decide -> decide_head) and the last
+// head of a group plans the group.
+constexpr int kDenseRows = 128;
+template <int kQDims>
+__global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, int ntarget) {
+  constexpr int SPR = kQDims / 8;
+  constexpr int NR = (128 - kQDims) / 8;
+  constexpr int LR = NR <= 8 ? 8 : 16;
+  constexpr int G = 32 / LR;
+  constexpr int RK = 32 / G;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Workspace ws = workspace_layout(p);
+  const int n_dense = (int)__ldcg(ws_ptr<const unsigned int>(p, ws.ctr_off) + 8);
+  const int W = p.window, nch = (W + kDenseRows - 1) / kDenseRows;
+  const int ci = lane % LR, gi = lane / LR;
+  const bool cload = ci < NR;
+  for (int task = blockIdx.x * (blockDim.x >> 5) + warp; task < n_dense * nch; task += gridDim.x * (blockDim.x >> 5)) {
+    const int bh = __ldcg(ws_ptr<const int>(p, ws.dlist_off) + task / nch);
+    const int chunk = task % nch;
+    const int4 st = __ldcg(ws_ptr<const int4>(p, ws.dstate_off) + bh);
+    const float D = __uint_as_float((unsigned)st.x);
+    const int cs1 = st.y, cs2 = st.z;
+    const int b = bh / p.n_q_heads;
+    const int m = p.seq_lens[b] + 1;
+    int first = m - W;
+    if (first < 1) first = 1;
+    if (p.delta_max > 0 && m - p.delta_max > first) first = m - p.delta_max;
+    const int last = m - 1;
+    const int n_scan = last >= first ? last - first + 1 : 0;
+    const int cur_slot = last >= 1 ? (last - 1) % W : 0;
+    const float* hpart = ws_ptr<const float>(p, ws.hpart_off) + (int64_t)bh * W;
+    const uint4* ring = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ring_q) + (int64_t)bh * W * 128);
+    float qh[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      qh[i] = cload ? (float)load_in(p.q_pre, (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
+    unsigned long long key = 0ull;
+    const int r0 = chunk * kDenseRows, r1 = min(W, r0 + kDenseRows);
+#pragma unroll 1
+    for (int base = r0; base < r1; base += 32) {
+      const float pr = base + lane < r1 ? __ldcg(hpart + base + lane) : CUDART_INF_F;
+      uint4 rv[RK];
+#pragma unroll
+      for (int k = 0; k < RK; ++k) {
+        const int slot = base + gi + G * k;
+        rv[k] = (slot < r1 && cload) ? ld_stream(ring + (int64_t)slot * 16 + SPR + ci) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < RK; ++k) {
+        float e = cload ? dist8(qh, rv[k]) : 0.f;
+#pragma unroll
+        for (int o = LR / 2; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        const int slot = base + gi + G * k;
+        const float prs = __shfl_sync(0xffffffffu, pr, gi + G * k);
+        if (slot < r1 && ci == 0 && prs <= D && prs != CUDART_INF_F && slot != cs1 && slot != cs2) {
+          const int pos = last - cur_slot + slot - (slot > cur_slot ? W : 0);
+          const unsigned long long k2 =
+              ~(((unsigned long long)__float_as_uint(prs + e) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos));
+          key = k2 > key ? k2 : key;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other > key ? other : key;
+    }
+    if (lane == 0 && publish_key(p, bh, key) == (unsigned)nch - 1) {
+      const unsigned long long k3 = atomicExch(ws_ptr<unsigned long long>(p, ws.mkey_off) + bh, 0ull);
+      ws_ptr<unsigned int>(p, ws.marr_off)[bh] = 0u;
+      double bd = CUDART_INF;
+      int bp = -1;
+      if (k3) {
+        const unsigned long long raw = ~k3;
+        bd = (double)__uint_as_float((unsigned)(raw >> 32));
+        bp = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
+      }
+      decide_head(p, bh, m, n_scan, bp > 0, bd, bp, nb, ntarget);
+    }
+  }
+}
+
+cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148 * 4);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int nb = band_split(p);
+  const int nt = nb > 0 ? piece_target(p) : 0;
+  if (qdims == 16) return cudaLaunchKernelEx(&cfg, dense_kernel<16>, p, nb, nt);
+  if (qdims == 32) return cudaLaunchKernelEx(&cfg, dense_kernel<32>, p, nb, nt);
+  return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt);
+}
+
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads);
   cfg.blockDim = dim3(per_head ? 32 : 32 * (p.n_q_heads / p.n_kv_heads));
@@ -485,14 +606,15 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   cfg.numAttrs = 1;
   const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
   const int nt = nb > 0 ? piece_target(p) : 0;
+  const int defer = dense_deferred(p) ? 1 : 0;
   if (qdims == 16)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, append)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, append);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, defer)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, defer);
   if (qdims == 32)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, append)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, append);
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, append)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, append);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, defer)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, defer);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, defer)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, defer);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -548,6 +670,8 @@ static int front_variant() {
 bool verify_per_group(const MacDecodeParams& p) {
   return p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
 }
+// match_mode 2 (expected misses): the per-group verify defers dense heads to dense_kernel
+bool dense_deferred(const MacDecodeParams& p) { return p.match_mode == 2 && verify_per_group(p); }
 // whether a match launch of the fast front runs the two-pass scan + verify kernels: enough heads
 // to fill the SMs, and a ring of 512..1024 rows — on smaller rings the one-pass scan reads little
 // more and a head whose query has no near-repeat (every row survives pass 1) costs the verify a
@@ -567,20 +691,22 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const bool per_head = !per_group && p.batch * p.n_q_heads >= 148;
   const bool two_pass = do_match && front_two_pass(p);
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
-  // a whole two-pass step: the append rides in the verify kernel's prologue (verify_kernel)
-  const bool app_in_verify = two_pass && do_append && passes == 3 && !rotate_only && !plan;
-  const bool app_in_front = do_append && !app_in_verify;
+  // (the append stays in the scan grid: in the verify's prologue it ran behind the scan's DRAM
+  // queue and delayed the decisions — C3 +7 us, r02 timeline)
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
-  const int n_append = app_in_front ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
-  if (n_match + n_append + (app_in_verify ? 1 : 0) == 0) return cudaSuccess;
+  const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
+  if (n_match + n_append == 0) return cudaSuccess;
   if (passes & 1) {
     auto fn = (do_match && u.fn_planar && p.ring_qp) ? u.fn_planar : u.fn;
-    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, app_in_front ? 1 : 0, rotate_only, plan, 0);
+    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
-  if ((passes & 2) && u.two_pass && do_match)
-    return launch_verify(p, st, per_head, u.rows, u.qdims, app_in_verify ? 1 : 0);
+  if ((passes & 2) && u.two_pass && do_match) {
+    const cudaError_t e = launch_verify(p, st, per_head, u.rows, u.qdims);
+    if (e || !dense_deferred(p)) return e;
+    return launch_dense(p, st, u.qdims);
+  }
   return cudaSuccess;
 }
 

@@ -216,7 +216,7 @@ class BatchDecodeEngine:
         # associate it differently (one-pass: 8-dim lane chunks + xor tree; two-pass: 16 planar
         # dims + the other 112), so a near-tie below fp32 resolution (|Δd| ~ 1e-6 relative) may
         # resolve differently between them — inside SURVEY §8c's documented near-tie band, never
-        # elsewhere.  match_mode="two_pass" / "one_pass" pin the scan for bitwise reproducible
+        # elsewhere.  match_mode="two_pass" / "dense" / "one_pass" pin the scan for bitwise reproducible
         # decisions; "adaptive" (the default) trades that for speed on miss-heavy steps.
         self.match_mode = "adaptive"
         self._fb_host = self._fb_alias = None
@@ -633,19 +633,44 @@ class BatchDecodeEngine:
         P = P if P is not None else self.last_params
         return int(_lib.load().mac_match_path(P))
 
+    # miss fraction above which the adaptive engine takes the one-pass scan even where the dense
+    # kernel is available (profiles/r02/SUMMARY.md, "Miss regime")
+    DENSE_MAX_MISS = 0.5
+
     def _choose_match_mode(self):
-        """The step's match scan (MacDecodeParams.match_mode), fixed for all of its stages."""
+        """The step's match scan (MacDecodeParams.match_mode), fixed for all of its stages:
+        0 two-pass (the hit path), 2 two-pass with the dense walks of heads without a near-repeat
+        spread over the GPU (dense_kernel), 1 one-pass scan."""
         if self.match_mode == "one_pass":
             self._step_mode = 1
         elif self.match_mode == "two_pass" or self._fb_host is None:
             self._step_mode = 0
+        elif self.match_mode == "dense":
+            self._step_mode = 2
         else:
-            # two-pass only while misses are rare: a single head without a near-repeat makes its
-            # verify warp walk the whole ring (~100 us), and the verify ends when its last head does
-            # (C3 geometry at 16K: 10% misses 435 us two-pass vs full attention 338 us; 30% misses
-            # 602 us two-pass, 316 us one-pass)
+            # Plain two-pass only while misses are rare: a head without a near-repeat makes its
+            # verify warp walk the whole ring (~60 us), and the verify ends with its last head.
+            # With misses, the per-group verify geometry hands those walks to dense_kernel (mode 2);
+            # other geometries, and miss-dominated steps, take the one-pass scan.
             missed, heads = (int(x) for x in self._fb_host.tolist())
-            self._step_mode = 1 if heads > 0 and 100 * missed > heads else 0
+            f = missed / heads if heads > 0 else 0.0
+            if f * 100 <= 1.0:
+                self._step_mode = 0
+            elif f <= self.DENSE_MAX_MISS and self._dense_capable():
+                self._step_mode = 2
+            else:
+                self._step_mode = 1
+
+    def _dense_capable(self) -> bool:
+        cap = self.__dict__.get("_dense_cap")
+        if cap is None:
+            P = self._params(0, self.o_out, self.o_out, self.o_out, _lib.DT_BF16)
+            saved = P.match_mode
+            P.match_mode = 2
+            path = int(_lib.load().mac_match_path(P))
+            P.match_mode = saved
+            cap = self._dense_cap = path > 0 and bool(path & _lib.PATH_DENSE_KERNEL)
+        return cap
 
     def stage(self, name: str, layer: int, q_pre, k_pre, v, force_miss: bool = False):
         """Launch one stage (mac_append_kv | mac_match | mac_amend | mac_complete) — for profiling/tests."""
@@ -797,8 +822,12 @@ class StepGraph:
             P.match_mode = 0
             two = _lib.load().mac_match_path(P)
             modes = [0, 1] if two > 0 and two & _lib.PATH_TWO_PASS else [0]
+            if 1 in modes and eng._dense_capable():
+                modes.append(2)
         elif eng.match_mode == "one_pass":
             modes = [1]
+        elif eng.match_mode == "dense":
+            modes = [2]
         else:
             modes = [0]
         self.graphs = {}

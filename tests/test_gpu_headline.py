@@ -44,7 +44,10 @@ def _c3_state(B, n0, S, hq, hkv, W, r, rep_prob, seed0):
     return states, kfull, vfull
 
 
-def test_c3_geometry_two_pass_parity():
+@pytest.mark.parametrize("mode", ["two_pass", "dense"])
+def test_c3_geometry_two_pass_parity(mode):
+    """mode "dense" (match_mode 2): the ~30% heads without a near-repeat are walked by dense_kernel
+    across the GPU instead of by their verify warp — same decisions, same outputs."""
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, StepGraph, _lib
 
     B, hq, hkv, W, r = 32, 32, 8, 1024, 256
@@ -54,7 +57,7 @@ def test_c3_geometry_two_pass_parity():
     states, kfull, vfull = _c3_state(B, n0, S, hq, hkv, W, r, 0.7, 4000)
     cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, tau=0.45, storage="bf16")
     eng = BatchDecodeEngine(cfg, B, n0 + S + 8, page_perm_seed=17)
-    eng.match_mode = "two_pass"  # the bench's hit-path configuration, whatever the misses feedback says
+    eng.match_mode = mode  # pinned, whatever the misses feedback says
     eng.inject(0, torch.from_numpy(np.stack(kfull)).cuda(), torch.from_numpy(np.stack(vfull)).cuda(),
                torch.from_numpy(np.stack([s.ring_q for s in states])).cuda(),
                torch.from_numpy(np.stack([s.ring_acc for s in states])).cuda(),
@@ -79,7 +82,7 @@ def test_c3_geometry_two_pass_parity():
         else:
             if sg is None:
                 sg = StepGraph(eng, 0, out_dtype=torch.bfloat16)
-                assert sg.direct and list(sg.graphs) == [0]
+                assert sg.direct and list(sg.graphs) == [2 if mode == "dense" else 0]
             sg.q_host.copy_(qd.cpu())
             sg.k_host.copy_(kd.cpu())
             sg.v_host.copy_(vd.cpu())
@@ -87,6 +90,7 @@ def test_c3_geometry_two_pass_parity():
         torch.cuda.synchronize()
         path = eng.match_path()
         assert path & _lib.PATH_TWO_PASS and path & _lib.PATH_VERIFY_GROUP and path & _lib.PATH_AMEND_MMA, path
+        assert bool(path & _lib.PATH_DENSE_KERNEL) == (mode == "dense"), path
         assert (path >> 8) > 0, "the split band did not run"
         if s >= S_dec:
             assert eng.last_params.out_bf16 is not None
@@ -242,7 +246,7 @@ def test_adaptive_scan_choice_reaches_the_kernels():
     ref.match_mode = "one_pass"
     gr = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
     sg = StepGraph(gr, 0)
-    assert sorted(sg.graphs) == [0, 1]
+    assert sorted(sg.graphs) == [0, 1, 2]
     q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)
     k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)
     v = np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)
@@ -261,6 +265,37 @@ def test_adaptive_scan_choice_reaches_the_kernels():
         torch.cuda.synchronize()
         assert torch.equal(res.match_pos, r2.match_pos) and torch.equal(res.match_hit, r2.match_hit), m
         assert torch.equal(sg.out_host, res.out.cpu()), m
-    assert paths[0] & _lib.PATH_TWO_PASS
+    assert paths[0] & _lib.PATH_TWO_PASS and not paths[0] & _lib.PATH_DENSE_KERNEL
+    # ~90% of the heads miss: past DENSE_MAX_MISS the engine takes the one-pass scan
     assert any(not (p & _lib.PATH_TWO_PASS) for p in paths), "the one-pass scan never ran"
     assert 1 in gmodes
+
+
+def test_adaptive_dense_mode_on_a_mixed_stream():
+    """~20% of the heads without a near-repeat on the per-group verify geometry: the adaptive engine
+    moves from the plain two-pass scan to match_mode 2 (dense_kernel walks the missing heads) and
+    stays bit-identical in decisions to a one-pass engine, outputs within 1e-4 of it."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic, _lib
+
+    B, hq, hkv, L, W, r = 37, 16, 4, 48, 512, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=900 + s,
+                                       rep_prob=0.8)) for s in range(B)]
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    ref = BatchDecodeEngine(cfg, B, L + 8, min_chunk=32)
+    ref.match_mode = "one_pass"
+    q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)
+    k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)
+    v = np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)
+    modes, worst = [], 0.0
+    for m in range(1, L + 1):
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a[m - 1])).to("cuda", torch.bfloat16)  # noqa: E731
+        res = eng.decode_step(0, dev(q), dev(k), dev(v))
+        modes.append((eng._step_mode, eng.match_path()))
+        r2 = ref.decode_step(0, dev(q), dev(k), dev(v))
+        assert torch.equal(res.match_hit, r2.match_hit) and torch.equal(res.match_pos, r2.match_pos), m
+        d = ((res.out - r2.out).norm(dim=-1) / r2.out.norm(dim=-1)).max().item()
+        worst = max(worst, d)
+    assert modes[0][0] == 0 and any(mm == 2 for mm, _ in modes), modes
+    assert any(p & _lib.PATH_DENSE_KERNEL for mm, p in modes if mm == 2)
+    assert worst <= TOL, worst

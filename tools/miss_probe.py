@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--miss-frac", type=float, default=1.0, help="fraction of heads given a fresh query")
-    ap.add_argument("--mode", default="adaptive", choices=("adaptive", "two_pass", "one_pass"))
+    ap.add_argument("--mode", default="adaptive", choices=("adaptive", "two_pass", "one_pass", "dense"))
     a = ap.parse_args()
     import bench
 
