@@ -13,7 +13,8 @@ import json
 import sys
 
 STAGES = {"front_half_kernel": "mac_match_scan", "front_bf16_d128_kernel": "mac_match_scan",
-          "verify_kernel": "mac_match_verify", "amend_mma_kernel": "mac_amend", "complete_bf16_kernel": "mac_complete"}
+          "verify_kernel": "mac_match_verify", "amend_mma_kernel": "mac_amend", "amend_tma_kernel": "mac_amend",
+          "dense_kernel": "mac_match_verify", "complete_bf16_kernel": "mac_complete"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
