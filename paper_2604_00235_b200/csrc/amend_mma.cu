@@ -116,10 +116,12 @@ struct AmendVariant {
   int smem;
 };
 static const AmendVariant kAmendVariants[] = {
-    {amend_mma_kernel<4, 7>, 4 * 2 * TILE_BYTES},
+    {amend_mma_kernel<4, 7>, 4 * 2 * TILE_BYTES},  // 0: the hit step
+    {amend_mma_kernel<3, 8>, 3 * 2 * TILE_BYTES},  // 1: full spans
+#ifdef MAC_DEV_KNOBS
     {amend_mma_kernel<6, 4>, 6 * 2 * TILE_BYTES},
     {amend_mma_kernel<2, 8>, 2 * 2 * TILE_BYTES},
-    {amend_mma_kernel<3, 8>, 3 * 2 * TILE_BYTES},
+#endif
 };
 constexpr int kAmendN = (int)(sizeof(kAmendVariants) / sizeof(kAmendVariants[0]));
 
@@ -137,7 +139,7 @@ static int amend_variant(bool full_spans) {
   }
   if (forced >= 0) return forced;
 #endif
-  return full_spans ? 3 : 0;
+  return full_spans ? 1 : 0;
 }
 
 // resident warps of a variant's persistent grid (sets the smem attribute on first use)
@@ -156,12 +158,6 @@ static int amend_grid_full(int vi, cudaError_t* err) {
   return grid_full[vi];
 }
 
-// Band items per GQA group for the split band (common.cuh band_items), 0 when the step does
-// not split it: the hit step of the fast path only — the two-pass front (whose verify kernel
-// the band overlaps, and which guarantees the append finished before this grid launches),
-// one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
-// (1..4).  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
-// kernel's plan and this launch call it with the same parameters, so they always agree.
 // Which kernel runs the hit step's amend.  With fewer GQA groups than SMs (C2: B = 8, 8 KV heads)
 // each group's items are long and few, and the one-warp kernel streams an item at ~5 GB/s per
 // warp (its 2-stage lookahead covers one DRAM round trip per 32 tokens), so the TMA kernel
@@ -187,6 +183,12 @@ static bool hit_amend_tma(const MacDecodeParams& p) {
 
 bool amend_uses_tma(const MacDecodeParams& p) { return hit_amend_tma(p); }
 
+// Band items per GQA group for the split band (common.cuh band_items), 0 when the step does
+// not split it: the hit step of the fast path only — the two-pass front (whose verify kernel
+// the band overlaps, and which guarantees the append finished before this grid launches),
+// one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
+// (1..4).  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
+// kernel's plan and this launch call it with the same parameters, so they always agree.
 int band_split(const MacDecodeParams& p) {
 #ifdef MAC_DEV_KNOBS
   static int forced = -2;

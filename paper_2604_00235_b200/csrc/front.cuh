@@ -12,46 +12,13 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
-// append + RoPE for one (request, kv head) by one warp; optionally plan the group as "all heads miss".
-// Every input load (seq_lens, the step's k / v / q rows, the RoPE frequencies) is issued before
-// any of them is used, so the warp pays two dependent memory round trips (those loads, then the
-// page-table entry of position m) — it runs beside a DRAM-saturating scan, where each round trip
-// costs ~1.5-2 us (C2: the dependent-load version ended the front grid 4.5 us after the scan).
+// append + RoPE for one (request, kv head) by one warp; optionally plan the group as "all heads miss"
 __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, int rotate_only, int plan) {
   const int lane = threadIdx.x & 31;
   const int b = idx / p.n_kv_heads, kvh = idx % p.n_kv_heads;
   const int g = p.n_q_heads / p.n_kv_heads;
   const Workspace w = workspace_layout(p);
-  __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);
-  __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(p.v_cache);
-  float* qrot = ws_ptr<float>(p, w.qrot_off);
-  // ---- round trip 1: everything that does not depend on m ----
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
-  const int dt = p.in_dtype;
-  const int64_t kbase = ((int64_t)b * p.n_kv_heads + kvh) * 128;
-  double fr[2], kx[2][2], vx[4];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int j = lane + 32 * u;
-    fr[u] = p.rope_freqs[j];
-    kx[u][0] = rotate_only ? 0.0 : load_in(p.k_pre, kbase + 2 * j, dt);
-    kx[u][1] = rotate_only ? 0.0 : load_in(p.k_pre, kbase + 2 * j + 1, dt);
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) vx[e] = rotate_only ? 0.0 : load_in(p.v_in, kbase + lane + 32 * e, dt);
-  constexpr int kMaxG = 4;  // query heads held in registers per pass (more: further passes)
-  float qx[kMaxG][2][2];
-  auto load_q = [&](int h0) {
-#pragma unroll
-    for (int t = 0; t < kMaxG; ++t)
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * (lane + 32 * u);
-        qx[t][u][0] = h0 + t < g ? (float)load_in(p.q_pre, qi, dt) : 0.f;
-        qx[t][u][1] = h0 + t < g ? (float)load_in(p.q_pre, qi + 1, dt) : 0.f;
-      }
-  };
-  load_q(0);
   if (lane == 0) ws_ptr<int>(p, w.mpos_off)[b] = m;  // every group's warp (same value)
   // every 8th token: the misses counted since the last publication (complete.cu) -> host.  Not
   // every step: a kernel that stores to host memory pays for the flush when it ends (~1 us).
@@ -64,7 +31,6 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
     ctr[4] = 0u;
     ctr[6] = 0u;
   }
-  // ---- round trip 2: the page of position m ----
   const int t_local = m - p.kv_offset;
   bool store = !rotate_only && t_local >= 1 && (p.kv_limit <= 0 || t_local <= p.kv_limit);
   if (store && !kv_fits(p.pages_per_seq, t_local, p.page_size)) {
@@ -73,36 +39,53 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
   }
   int64_t row = 0;
   if (store) row = kv_row(p.page_table, p.pages_per_seq, b, t_local, p.page_size, p.n_kv_heads, kvh);
-  double sn[2], cs[2];
+  __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);
+  __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(p.v_cache);
+  float* qrot = ws_ptr<float>(p, w.qrot_off);
+  // bf16 / f32 inputs (exact in fp32 registers): each head's query pair used to be loaded after
+  // the previous head's store — a memory round trip per head, which made the append warps, not
+  // the scan, end the front kernel (C2: the verify waited 6.7 us past the last scan CTA)
+  const bool batch = p.in_dtype != MAC_DT_F64;
+  for (int j = lane; j < 64; j += 32) {
+    double s, c;
+    sincos((double)m * p.rope_freqs[j], &s, &c);
+    if (store) {
+      const int64_t ki = ((int64_t)b * p.n_kv_heads + kvh) * 128 + 2 * j;
+      const double x0 = load_in(p.k_pre, ki, p.in_dtype), x1 = load_in(p.k_pre, ki + 1, p.in_dtype);
+      __nv_bfloat162 kk;
+      kk.x = from_f64<__nv_bfloat16>(x0 * c - x1 * s);
+      kk.y = from_f64<__nv_bfloat16>(x0 * s + x1 * c);
+      reinterpret_cast<__nv_bfloat162*>(kc + row * 128)[j] = kk;
+    }
+    if (batch) {  // four heads' query pairs in flight together, then their stores
+      for (int h0 = 0; h0 < g; h0 += 4) {
+        float xa[4], xb[4];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) sincos((double)m * fr[u], &sn[u], &cs[u]);
-  // rotated queries (fp64 angles, fp32 storage) need no page: stored first
-  for (int h0 = 0; h0 < g; h0 += kMaxG) {
-    if (h0 > 0) load_q(h0);
+        for (int t = 0; t < 4; ++t) {
+          const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
+          xa[t] = h0 + t < g ? (float)load_in(p.q_pre, qi, p.in_dtype) : 0.f;
+          xb[t] = h0 + t < g ? (float)load_in(p.q_pre, qi + 1, p.in_dtype) : 0.f;
+        }
 #pragma unroll
-    for (int t = 0; t < kMaxG; ++t) {
-      if (h0 + t >= g) break;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * (lane + 32 * u);
-        const double x0 = qx[t][u][0], x1 = qx[t][u][1];
-        reinterpret_cast<float2*>(qrot + qi)[0] =
-            make_float2((float)(x0 * cs[u] - x1 * sn[u]), (float)(x0 * sn[u] + x1 * cs[u]));
+        for (int t = 0; t < 4; ++t) {
+          if (h0 + t >= g) break;
+          const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
+          const double x0 = xa[t], x1 = xb[t];
+          reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+        }
+      }
+    } else {
+      for (int hl = 0; hl < g; ++hl) {
+        const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
+        const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
+        reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
       }
     }
   }
-  if (store) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = lane + 32 * u;
-      __nv_bfloat162 kk;
-      kk.x = from_f64<__nv_bfloat16>(kx[u][0] * cs[u] - kx[u][1] * sn[u]);
-      kk.y = from_f64<__nv_bfloat16>(kx[u][0] * sn[u] + kx[u][1] * cs[u]);
-      reinterpret_cast<__nv_bfloat162*>(kc + row * 128)[j] = kk;
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) vc[row * 128 + lane + 32 * e] = from_f64<__nv_bfloat16>(vx[e]);
-  }
+  if (store)
+    for (int e = lane; e < 128; e += 32)
+      vc[row * 128 + e] =
+          from_f64<__nv_bfloat16>(load_in(p.v_in, ((int64_t)b * p.n_kv_heads + kvh) * 128 + e, p.in_dtype));
   if (plan && lane == 0) {
     int* lo = ws_ptr<int>(p, w.lo_off);
     for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;
