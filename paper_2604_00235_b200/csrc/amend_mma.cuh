@@ -368,10 +368,6 @@ __device__ __forceinline__ void amend_mma_item(const MacDecodeParams& p, int4 it
     S.reset();
   }
   write_partial(S, out, 1, row, q4, g);
-  // publish the item: the complete kernel merges the group once all of its items counted
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) atomicAdd(ws_ptr<unsigned>(p, w.gdone_off) + grp, 1u);
 }
 
 }  // namespace mac

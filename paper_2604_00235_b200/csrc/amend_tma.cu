@@ -357,9 +357,7 @@ __global__ void __launch_bounds__(TmaRing<TA_NC, TA_NS>::THREADS, MINB)
       }
       if (lane == 0) out[hs * 129 + 128] = Z > 0.f ? L + __logf(Z) : -CUDART_INF_F;
     }
-    __threadfence();
-    consumers_sync<TA_NC>();  // scratch free for the next item; the item's partials are out
-    if (cw == 0 && lane == 0) atomicAdd(ws_ptr<unsigned>(p, w.gdone_off) + grp, 1u);  // publish
+    consumers_sync<TA_NC>();  // scratch free for the next item
     if (lane == 0) mbar_arrive(bar_dempty + 8 * ds);
   }
   if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");

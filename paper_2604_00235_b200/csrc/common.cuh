@@ -102,11 +102,6 @@ __device__ __forceinline__ double fexpm1(double x) { return expm1(x); }
 
 // gpu-scope acquire-release fetch-add: orders this thread's earlier writes before
 // the increment and later reads after it (replaces a fence + atomicAdd pair)
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -272,11 +267,8 @@ struct Workspace {
                      //              (complete adds; every 8th step's append warps publish and reset)
                      //              2 KV overflow flag (an append found no page for its token; sticky)
                      //              8 dense heads deferred by the verify (match_mode 2; reset by complete)
-                     //              3 sticky: a complete gave up waiting for its group's items (2 s)
-                     //              (5, 7, 9-15 spare)
-  size_t gdone_off;  // [B*Hkv] u32  work items of the group whose partials are published (bf16 amends
-                     //              add, released; complete_bf16_kernel polls; the step's append
-                     //              warps zero it — one per group — before any amend can start)
+                     //              (3, 5, 7, 9-15 spare)
+  size_t gdone_off;  // [B*Hkv] u32  splits of the group finished (fused complete)
   size_t pn_off;     // [B*Hkv] i32  piece splits planned for the group | band items requested << 16
   size_t mpos_off;   // [B] i32      position m of this step
   size_t lo_off;     // [B*Hq] i32   first token each head reads (plan)

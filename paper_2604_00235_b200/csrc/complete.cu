@@ -36,13 +36,19 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
   const int bh = blockIdx.x * 4 + (threadIdx.x >> 5);
   const Workspace wsl = workspace_layout(p);
   const bool live = bh < p.batch * p.n_q_heads;
-  // Everything read before the partials was written by kernels that finished before this grid
-  // could launch (the front and verify kernels; earlier steps for the ring), so hop A and the
-  // cached ring summary load while the amend kernel drains (L2 loads: nothing stale in L1).
-  // The partials are read per GQA group, as soon as the group's last work item has published
-  // them (gdone, an acquire poll) — not after the whole amend grid: the merges of early groups
-  // overlap the amend's tail, and the step ends one merge after the last item instead of a
-  // grid drain plus a merge.
+  // Everything before the grid-dependency wait was written by kernels that finished before
+  // this grid could launch (the front and verify kernels; earlier steps for the ring), so
+  // hop A and the cached ring summary load while the amend kernel drains (L2 loads: nothing
+  // stale in L1).  Only the amend's partials are read after the wait.
+  if (!live) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+      ctr[8] = 0u;
+    }
+  }
   if (live) {
     const float NINF = -CUDART_INF_F;
     const int b = bh / p.n_q_heads, h = bh % p.n_q_heads;
@@ -79,22 +85,14 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
     float aacc[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) aacc[k] = use ? __ldcg(racc + cslot * 128 + lane + 32 * k) : 0.f;
-    if (lane == 0) {  // the group's nsl work items have all published their partials
-      const unsigned* gd = ws_ptr<const unsigned>(p, wsl.gdone_off) + grp;
-      unsigned long long t0;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      while (ld_acquire_gpu(gd) < (unsigned)nsl) {
-        __nanosleep(32);
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 2000000000ull) {  // 2 s: a protocol bug, never a wait — flag it, do not hang
-          atomicOr(ws_ptr<unsigned>(p, wsl.ctr_off) + 3, 1u);
-          break;
-        }
-      }
-    }
-    __syncwarp();
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     TL_MARK(p, TL_COMPLETE_WAITED);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // work list consumed: list length and amend claim counter
+      unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+      ctr[8] = 0u;
+    }
     float Mp = NINF, Sp = 0.f, Mb = NINF, Sb = 0.f, ap[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
     for (int cb = 0; cb < nsl; cb += 8) {
       float lp[8], lb[8], xp[8][4], xb[8][4];
@@ -222,15 +220,6 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
     if (live && lane == 0 && !__ldcg(p.match_hit + bh)) atomicAdd(ws_ptr<unsigned>(p, wsl.ctr_off) + 4, 1u);
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ws_ptr<unsigned>(p, wsl.ctr_off) + 6, 1u);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    // the work list and the amend's claim counter are reused next step: reset them once the
-    // whole amend grid is done (late warps still make one last, empty claim)
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    unsigned int* ctr = ws_ptr<unsigned int>(p, wsl.ctr_off);
-    ctr[0] = 0u;
-    ctr[1] = 0u;
-    ctr[8] = 0u;
-  }
 #ifdef MAC_TIMELINE
   __syncthreads();
 #endif
@@ -248,10 +237,7 @@ cudaError_t launch_complete(const MacDecodeParams& p, cudaStream_t st, int full_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // complete_bf16_kernel waits on the items the bf16 tensor-core amends publish (gdone): only
-  // with those amends (amend_mma_supported), and only for the unsharded ring step
-  if (MODE == MAC_MODE_BF16 && full_mode == COMPLETE_RING && p.head_dim == 128 && p.head_dim_v == 128 &&
-      amend_mma_supported(p) && p.n_shards == 0)
+  if (MODE == MAC_MODE_BF16 && full_mode == COMPLETE_RING && p.head_dim == 128 && p.head_dim_v == 128)
     return cudaLaunchKernelEx(&cfg, complete_bf16_kernel, p);
   return cudaLaunchKernelEx(&cfg, complete_kernel<MODE>, p, full_mode);
 }

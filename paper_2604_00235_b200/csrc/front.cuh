@@ -19,10 +19,7 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
   const int g = p.n_q_heads / p.n_kv_heads;
   const Workspace w = workspace_layout(p);
   const int m = p.seq_lens[b] + (rotate_only ? 0 : 1);
-  if (lane == 0) {
-    ws_ptr<int>(p, w.mpos_off)[b] = m;  // every group's warp (same value)
-    ws_ptr<unsigned>(p, w.gdone_off)[idx] = 0u;  // this step's published-items count of the group
-  }
+  if (lane == 0) ws_ptr<int>(p, w.mpos_off)[b] = m;  // every group's warp (same value)
   // every 8th token: the misses counted since the last publication (complete.cu) -> host.  Not
   // every step: a kernel that stores to host memory pays for the flush when it ends (~1 us).
   // With several layers per token every layer's complete counts into the same counters and only

@@ -336,13 +336,6 @@ class BatchDecodeEngine:
                                                                     _lib.DT_F32)))
         return int(self.workspace[off:off + 4].view(torch.int32).item()) != 0
 
-    def check_protocol(self) -> bool:
-        """True when a complete kernel ever gave up waiting (2 s) for its group's amend items —
-        a device-side protocol error that is flagged instead of hanging (synchronises)."""
-        off = int(_lib.load().mac_overflow_flag_offset(self._params(0, self.o_out, self.o_out, self.o_out,
-                                                                    _lib.DT_F32))) + 4
-        return int(self.workspace[off:off + 4].view(torch.int32).item()) != 0
-
     # ------------------------------------------------------------------ launch
     def _params(self, layer: int, q, k, v, in_dt: int, force_miss: bool = False) -> _lib.MacDecodeParams:
         key = (layer, q.data_ptr(), k.data_ptr(), v.data_ptr(), in_dt, force_miss)

@@ -119,7 +119,7 @@ def test_c3_geometry_two_pass_parity(mode):
     assert worst["out_bf16"] <= 8e-3, worst  # one bf16 rounding (2^-8 relative) of a <= 1e-4 result
     assert torch.equal(eng.ring_qp[0], eng.ring_q[0][..., :_lib.PLANAR_DIMS])
     assert eng.seq_lens[0].tolist() == [n0 + S] * B
-    assert not eng.check_overflow() and not eng.check_protocol()
+    assert not eng.check_overflow()
 
 
 @pytest.mark.parametrize("rep_prob,noise_eps", [(1.0, 0.0), (0.9, 0.1)])
