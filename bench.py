@@ -546,10 +546,11 @@ def run_ours(args, wl):
     dom = max(("mac_match_scan", "mac_amend"), key=lambda n: kern[n]["bytes"])
     step_gbs = mean_b["total"] / (ms_per_step * 1e-3) / 1e9
 
-    sub_rec = None
+    sub_rec = mix_rec = None
     if sub is not None:
         del sg
         sub_rec = measure_sub(args, dev, *sub)
+        mix_rec = measure_mix(args, dev)
 
     result = None
     if rank == 0:
@@ -613,6 +614,8 @@ def run_ours(args, wl):
         }
         if sub_rec is not None:
             result["c2"] = sub_rec
+        if mix_rec is not None:
+            result["c3mix"] = mix_rec
         if cpu is not None:
             result["cpu_baseline"] = {"value": cpu["tokens_per_s"], "unit": "tokens/s", "cores": procs, "kind": "port",
                                       "sample": f"{procs} requests x {args.cpu_steps} steps of this workload "
@@ -683,6 +686,70 @@ def measure_sub(args, dev, wl, n0, S, states):
     del eng
     torch.cuda.empty_cache()
     return rec
+
+
+def measure_mix(args, dev):
+    """The mixed regime at the C3 geometry (B = 32, 32Q/8KV, W = 1024, r = 256) and a 16K context:
+    a fraction of the heads gets a fresh query (no near-repeat: it misses, and its GQA group reads
+    the whole context), the rest near-repeats.  The default (adaptive) engine's device time per
+    step after it has adapted (the second half of each run) vs full-attention decode on the same
+    state; L2 flushed before every step (tools/miss_probe.py protocol)."""
+    import torch
+
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig
+    from paper_2604_00235_b200.synth import inject_into_engine
+
+    ctx, B, hq, hkv, S = 16384, 32, 32, 8, 24
+    fracs = (0.02, 0.1, 0.3)
+    n0 = ctx - len(fracs) * S - 16
+    states = make_states(list(range(20_000, 20_000 + B)), n0=n0, steps=S, hq=hq, hkv=hkv, d=D, dv=D, window=WINDOW,
+                         band=BAND)
+    cfg = EngineConfig(d=D, d_v=D, n_q_heads=hq, n_kv_heads=hkv, window=WINDOW, band=BAND, tau=TAU, storage="bf16")
+    eng = BatchDecodeEngine(cfg, B, ctx + 64, device=dev)
+    inject_into_engine(eng, 0, states, n0, bulk_seed=5)
+    g = torch.Generator(device=dev).manual_seed(11)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    q_rep = torch.from_numpy(np.stack([st.step_q for st in states], 1)).to(dev, torch.bfloat16)
+    out = {"workload": "C3 geometry (B=32, 32Q/8KV, W=1024, r=256), 16K context, a fraction of heads with fresh "
+                       "queries; adaptive engine, steady state", "context": ctx}
+    for frac in fracs:
+        ts, miss, modes = [], [], []
+        for s in range(S):
+            fresh = torch.randn(B, hq, D, device=dev, generator=g).bfloat16()
+            pick = torch.rand(B, hq, 1, device=dev, generator=g) < frac
+            q = torch.where(pick, fresh, q_rep[s])
+            k = torch.randn(B, hkv, D, device=dev, generator=g).bfloat16()
+            v = torch.randn(B, hkv, D, device=dev, generator=g).bfloat16()
+            l2_flush(flush)
+            torch.cuda._sleep(200_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.decode_step(0, q, k, v)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if s >= S // 2:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+                miss.append(1.0 - float(eng.o_use.float().mean()))
+                modes.append(int(eng._step_mode))
+        out[f"miss_{frac}"] = {"mac_us": float(np.mean(ts)), "miss_rate": float(np.mean(miss)),
+                               "match_modes": sorted(set(modes))}
+    fts = []
+    for s in range(5):
+        l2_flush(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.full_decode(0, q_rep[s], q_rep[s][:, :hkv].contiguous(), q_rep[s][:, :hkv].contiguous())
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if s >= 2:
+            fts.append(e0.elapsed_time(e1) * 1e3)
+    out["full_attention_us"] = float(np.mean(fts))
+    for frac in fracs:
+        out[f"miss_{frac}"]["vs_full_attention"] = out[f"miss_{frac}"]["mac_us"] / out["full_attention_us"]
+    del eng
+    torch.cuda.empty_cache()
+    return out
 
 
 # ----------------------------------------------------------------------------
