@@ -158,34 +158,10 @@ __device__ __forceinline__ float dist8_f2(const unsigned long long* q2, uint4 c)
 // distance is the one-pass kernel's fp32 sum of squares split in two sums.
 // PLANAR (kQDims = MAC_PLANAR_DIMS = 16): the rows are read from ring_qp, 32 contiguous bytes
 // per row (a contiguous 32 KiB stream per head) instead of strided prefixes of ring_q.
-// L2 prefetch of the K/V rows a hit step will read whatever the match decides: the band
-// [m-r+1, m] and the last `tokens` positions of the piece [.., m-r] (the piece always ends at
-// m-r; its start is the match's).  Issued by the append warps of the two-pass scan grid
-// (cp.async.bulk.prefetch.L2, one 16-token sub-tile of K and of V per instruction), so those
-// bytes move while the scan and the verify leave the DRAM underused; the amend then finds them
-// in L2.  One warp per (request, kv head).
-__device__ __forceinline__ void prefetch_group_kv(const MacDecodeParams& p, int idx, int tokens) {
-  const int lane = threadIdx.x & 31;
-  const int b = idx / p.n_kv_heads, kvh = idx % p.n_kv_heads;
-  const int m = p.seq_lens[b] + 1;
-  int t0 = m - p.band - tokens + 1;
-  t0 = t0 < 1 ? 1 : t0;
-  t0 = ((t0 - 1) & ~15) + 1;  // 16-token sub-tiles (page_size % 16 == 0)
-  const int nsub = (m - t0) / 16 + 1;
-  const char* kc = static_cast<const char*>(p.k_cache);
-  const char* vc = static_cast<const char*>(p.v_cache);
-  for (int j = lane; j < nsub; j += 32) {
-    const int t = t0 + 16 * j;
-    const int64_t row = kv_row(p.page_table, p.pages_per_seq, b, t, p.page_size, p.n_kv_heads, kvh);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], 4096;" ::"l"(kc + row * 256) : "memory");
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], 4096;" ::"l"(vc + row * 256) : "memory");
-  }
-}
-
 template <int kRowsPerCta, int kMinBlocks, int kQDims, bool PLANAR = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDecodeParams p, int n_match,
                                                                           int do_append, int rotate_only, int plan,
-                                                                          int prefetch) {
+                                                                          int /*unused*/) {
   constexpr int LPR = kQDims / 8;                    // lanes per row (16 B = 8 dims each)
   constexpr int RPW = 32 / LPR;                      // rows per warp-load
   constexpr int kLoads = kRowsPerCta / (8 * RPW);    // loads per lane
@@ -197,10 +173,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   TL_MARK(p, TL_SCAN_IN);
   if ((int)blockIdx.x < n_append) {
     const int i = blockIdx.x * (kThreads / 32) + warp;
-    if (i < p.batch * p.n_kv_heads) {
-      append_warp(p, i, rotate_only, plan);
-      if (prefetch > 0) prefetch_group_kv(p, i, prefetch);
-    }
+    if (i < p.batch * p.n_kv_heads) append_warp(p, i, rotate_only, plan);
     return;
   }
   const int W = p.window;
@@ -694,20 +667,6 @@ static int front_variant() {
   return 0;
 #endif
 }
-// piece tokens the two-pass scan grid prefetches into L2 per group (beside the band);
-// development builds sweep it with MAC_PREFETCH_TOKENS
-static int prefetch_tokens() {
-#ifdef MAC_DEV_KNOBS
-  static int v = -2;
-  if (v == -2) {
-    const char* env = getenv("MAC_PREFETCH_TOKENS");
-    v = env ? atoi(env) : -1;
-  }
-  if (v >= 0) return v;
-#endif
-  return 256;
-}
-
 bool verify_per_group(const MacDecodeParams& p) {
   return p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
 }
@@ -739,9 +698,7 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   if (n_match + n_append == 0) return cudaSuccess;
   if (passes & 1) {
     auto fn = (do_match && u.fn_planar && p.ring_qp) ? u.fn_planar : u.fn;
-    // L2 prefetch of the hit step's certain K/V (two-pass scan with the split band only)
-    const int pf = (two_pass && do_append && !rotate_only && !plan && band_split(p) > 0) ? prefetch_tokens() : 0;
-    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, pf);
+    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
