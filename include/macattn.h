@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 10
+#define MACATTN_ABI_VERSION 11
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -261,6 +261,7 @@ typedef struct MacRingBuildParams {
   int32_t n_rows;     /* 1 .. min(window, seq_lens[b]) */
   int32_t n_chunks;   /* key splits per row block (>= 1); > 1 needs `part` */
   void* part;         /* [B, n_rows, Hq, n_chunks, d_v + 1] f32 scratch (NULL when n_chunks == 1) */
+  int32_t variant;    /* 0: tcgen05 kernel where supported (else mma.sync), 1: mma.sync, 2: tcgen05 */
 } MacRingBuildParams;
 
 int mac_abi_version(void);

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 10
+ABI_VERSION = 11
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -193,7 +193,7 @@ class MacMatchRowsParams(C.Structure):
 
 
 class MacRingBuildParams(C.Structure):
-    _fields_ = [("n_rows", C.c_int32), ("n_chunks", C.c_int32), ("part", C.c_void_p)]
+    _fields_ = [("n_rows", C.c_int32), ("n_chunks", C.c_int32), ("part", C.c_void_p), ("variant", C.c_int32)]
 
 
 _lib = None

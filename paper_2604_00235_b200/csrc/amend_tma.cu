@@ -382,7 +382,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // a [rows, 128] bf16 view of a paged cache ([num_pages, Hkv, page_size, 128]: one row per
 // (page, kv head, slot)), 64 x 16 boxes, 128-byte swizzle.  The row count only bounds the
 // coordinates (every coordinate the kernel issues lies inside the caller's allocation).
-static bool encode_cache_map(CUtensorMap* m, const void* ptr) {
+bool encode_cache_map(CUtensorMap* m, const void* ptr) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {128, (cuuint64_t)1 << 31};

@@ -19,7 +19,7 @@ bool front_fast_supported(const MacDecodeParams&);
 cudaError_t launch_merge_partials(const MacMergeParams&, cudaStream_t);
 template <int MODE> cudaError_t launch_prefill_kv(const MacDecodeParams&, int, cudaStream_t);
 bool ring_build_supported(const MacDecodeParams&);
-cudaError_t launch_ring_build(const MacDecodeParams&, const MacRingBuildParams&, cudaStream_t);
+cudaError_t launch_ring_build(const MacDecodeParams&, const MacRingBuildParams&, cudaStream_t, int use_tc);
 template <int MODE> cudaError_t launch_step_stats(const MacDecodeParams&, double*, double*, cudaStream_t);
 template <int MODE> cudaError_t launch_mass_bound(const MacDecodeParams&, const MacMassBoundParams&, cudaStream_t);
 }  // namespace mac
@@ -215,7 +215,8 @@ int mac_build_ring(const MacDecodeParams* p, const MacRingBuildParams* rb, void*
   if (rb->n_rows < 0 || rb->n_rows > p->window || rb->n_chunks < 1) return MAC_ERR_SHAPE;
   if (rb->n_chunks > 1 && !rb->part) return MAC_ERR_NULL;
   if (rb->n_rows == 0) return MAC_OK;
-  return (int)launch_ring_build(*p, *rb, static_cast<cudaStream_t>(stream));
+  if (rb->variant < 0 || rb->variant > 2) return MAC_ERR_SHAPE;
+  return (int)launch_ring_build(*p, *rb, static_cast<cudaStream_t>(stream), rb->variant == 0 ? -1 : (rb->variant == 2 ? 1 : 0));
 }
 
 int mac_step_stats(const MacDecodeParams* p, double* head_stats, double* group_stats, void* stream) {

@@ -241,7 +241,19 @@ bool ring_build_supported(const MacDecodeParams& p) {
          p.page_size % 16 == 0 && p.kv_offset == 0 && p.kv_limit == 0;
 }
 
-cudaError_t launch_ring_build(const MacDecodeParams& p, const MacRingBuildParams& a, cudaStream_t st) {
+bool ring_build_tc_supported(const MacDecodeParams& p);
+cudaError_t launch_ring_build_tc(const MacDecodeParams& p, const MacRingBuildParams& a, cudaStream_t st);
+
+// the tcgen05 kernel (ring_build_tc.cu) where it applies, else this file's mma.sync kernel;
+// use_tc < 0: by support, 0 / 1: forced (tests compare the two)
+cudaError_t launch_ring_build(const MacDecodeParams& p, const MacRingBuildParams& a, cudaStream_t st, int use_tc) {
+  const bool tc = use_tc < 0 ? ring_build_tc_supported(p) : (use_tc > 0 && ring_build_tc_supported(p));
+  if (tc) {
+    cudaError_t e = launch_ring_build_tc(p, a, st);
+    if (e != cudaSuccess || a.n_chunks == 1) return e;
+    ring_merge_kernel<<<p.batch * a.n_rows * p.n_q_heads, 128, 0, st>>>(p, a);
+    return cudaGetLastError();
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(ring_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM);

@@ -1,0 +1,361 @@
+// Prefill ring construction on the 5th-generation tensor cores (tcgen05 / TMEM / TMA): the same
+// contract as ring_build.cu (the ring entries of the last n positions of a cached prompt,
+// slot (t-1) mod W <- (q_t, AS[1, t-r] under R_t q_t); engine.py:374-402, 484-499) computed as a
+// flash-attention pass with a causal lag of r, M = 128 query rows per CTA.
+//
+// CTA = (request, kv head, block of 128/g positions -> 128 rows = positions x g heads, key chunk).
+// Warp roles (192 threads):
+//   warps 0-3  one thread per row: rotate its query (fp64 angles), split it hi/lo into the two
+//              bf16 A operands; per 64-key tile read its S row from TMEM, online softmax in the
+//              log2 domain (lazy rescale: the reference max moves only by > 8), write P hi/lo
+//              (bf16) into shared memory, rescale its O row in TMEM when the max moved;
+//              epilogue O / Z and lse -> ring slot (or a chunk partial)
+//   warp 4     one elected thread issues the UMMAs: S = Q_hi K^T + Q_lo K^T (K-major A and B,
+//              M = 128, N = 64, fp32 in TMEM, double-buffered) and O += P_hi V + P_lo V (V
+//              MN-major, N = 128); tcgen05.commit signals S ready / P consumed / stage free
+//   warp 5     TMA producer: each 64-key tile is 4 pages x 2 dim halves of K and of V (2D tensor
+//              maps over the paged cache, SWIZZLE_128B = the UMMA canonical layout), 3 stages
+// The hi/lo splits keep the logits and P exact to fp32 (the parity the decode kernels hold, see
+// amend_mma.cuh); each MMA pair reads the same K or V tile.  Descriptor and TMEM layouts:
+// umma.cuh, validated against a host GEMM by tools/umma_probe.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace mac {
+
+bool encode_cache_map(CUtensorMap* m, const void* ptr);  // amend_tma.cu
+
+namespace {
+using namespace umma;
+constexpr int TC_THREADS = 192;
+constexpr int TC_NS = 3;                   // K/V stages
+constexpr int TC_TILE = 64;                // keys per tile
+constexpr int OFF_QHI = 0, OFF_QLO = 32768, OFF_PHI = 65536, OFF_PLO = 81920, OFF_KV = 98304;
+constexpr int KV_STAGE = 32768;            // K 16 KB (2 atoms x 64 keys x 128 B) + V 16 KB
+constexpr int OFF_BAR = OFF_KV + TC_NS * KV_STAGE;
+constexpr int TC_SMEM = OFF_BAR + 256 + 1024;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ uint32_t kmaj_off(int r, int k, int R) {
+  return (uint32_t)((k >> 6) * R * 128 + r * 128 + ((((k & 63) >> 3) ^ (r & 7)) << 4) + (k & 7) * 2);
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    ring_build_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                         MacDecodeParams p, MacRingBuildParams a) {
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char* sm = smem_raw + (base - raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Hkv = p.n_kv_heads, Hq = p.n_q_heads, g = Hq / Hkv, r = p.band, ps = p.page_size, W = p.window;
+  const int pb_rows = 128 / g;
+  const int n_pb = (a.n_rows + pb_rows - 1) / pb_rows;
+  int item = blockIdx.x;
+  const int ch = item % a.n_chunks;
+  item /= a.n_chunks;
+  const int pb = item % n_pb;
+  item /= n_pb;
+  const int kvh = item % Hkv, b = item / Hkv;
+  const int n = p.seq_lens[b];
+  const int first = n - a.n_rows + 1;
+  const int i0 = pb * pb_rows;
+  const int i_last = min(a.n_rows, i0 + pb_rows) - 1;
+  const int kmax = first + i_last - r;
+  const int span = kmax >= 1 ? (kmax + TC_TILE - 1) / TC_TILE : 0;
+  const int per = (span + a.n_chunks - 1) / a.n_chunks;
+  const int tile0 = ch * per, nt = max(0, min(span, tile0 + per) - tile0);
+  const int k0 = 1 + tile0 * TC_TILE, k1 = min(kmax, (tile0 + per) * TC_TILE);
+
+  const uint32_t bar = base + OFF_BAR;
+  const uint32_t b_full = bar, b_empty = bar + 8 * TC_NS, b_sfull = bar + 16 * TC_NS, b_pfull = b_sfull + 16,
+                 b_odone = b_pfull + 8, b_qfull = b_odone + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_BAR + 128);
+  if (tid == 0) {
+    for (int i = 0; i < TC_NS; ++i) {
+      mbar_init(b_full + 8 * i, 1);
+      mbar_init(b_empty + 8 * i, 1);
+    }
+    mbar_init(b_sfull, 1);
+    mbar_init(b_sfull + 8, 1);
+    mbar_init(b_pfull, 128);
+    mbar_init(b_odone, 1);
+    mbar_init(b_qfull, 128);
+    fence_mbar_init();
+  }
+  if (warp == 4) tmem_alloc(smem_u32(tmem_slot), 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = *tmem_slot;  // S buffers at columns 0 / 64, O at 128
+
+  if (warp == 5) {
+    // ------------------------------------------------------------------ TMA producer
+    for (int j = 0; j < nt; ++j) {
+      const int st = j % TC_NS;
+      // lane s < 4: the cache row of sub-tile s (16 keys inside one page)
+      int row = 0;
+      if (lane < 4) {
+        const int tok = k0 + j * TC_TILE + lane * 16;
+        const int pg = p.page_table[(int64_t)b * p.pages_per_seq + min((tok - 1) / ps, p.pages_per_seq - 1)];
+        row = (pg * Hkv + kvh) * ps + ((tok - 1) % ps);
+      }
+      const int r0 = __shfl_sync(0xffffffffu, row, 0), r1 = __shfl_sync(0xffffffffu, row, 1);
+      const int r2 = __shfl_sync(0xffffffffu, row, 2), r3 = __shfl_sync(0xffffffffu, row, 3);
+      if (lane == 0) {
+        mbar_wait_parity(b_empty + 8 * st, ((j / TC_NS) & 1) ^ 1);
+        const uint32_t fb = b_full + 8 * st;
+        mbar_expect_tx(fb, KV_STAGE);
+        const uint32_t ks = base + OFF_KV + st * KV_STAGE, vs = ks + 16384;
+        const int rows[4] = {r0, r1, r2, r3};
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            tma2d(ks + h * 8192 + s * 2048, &tmK, h * 64, rows[s], fb);
+            tma2d(vs + h * 8192 + s * 2048, &tmV, h * 64, rows[s], fb);
+          }
+      }
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------------------------ UMMA issuer
+    if (lane == 0 && nt > 0) {
+      const uint32_t idS = instr_desc_bf16(128, TC_TILE, false, false);
+      const uint32_t idO = instr_desc_bf16(128, 128, false, true);
+      const uint32_t qhi = base + OFF_QHI, qlo = base + OFF_QLO, phi = base + OFF_PHI, plo = base + OFF_PLO;
+      auto issue_s = [&](int j) {
+        const int st = j % TC_NS;
+        mbar_wait_parity(b_full + 8 * st, (j / TC_NS) & 1);
+        tc_fence_after();
+        const uint32_t ks = base + OFF_KV + st * KV_STAGE;
+        const uint32_t d = tm + (uint32_t)((j & 1) * TC_TILE);
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {  // 8 k-steps of the hi operand, then 8 of the lo operand
+          const int ks8 = kk & 7;
+          const uint32_t aoff = (ks8 >> 2) * 16384 + (ks8 & 3) * 32, boff = (ks8 >> 2) * 8192 + (ks8 & 3) * 32;
+          mma_bf16(d, sdesc_kmajor_sw128((kk < 8 ? qhi : qlo) + aoff), sdesc_kmajor_sw128(ks + boff), idS, kk > 0);
+        }
+        mma_commit(b_sfull + 8 * (j & 1));
+      };
+      mbar_wait_parity(b_qfull, 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < nt; ++j) {
+        if (j + 1 < nt) issue_s(j + 1);
+        mbar_wait_parity(b_pfull, j & 1);
+        tc_fence_after();
+        const uint32_t vs = base + OFF_KV + (j % TC_NS) * KV_STAGE + 16384;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // P_hi . V then P_lo . V, 4 k-steps of 16 keys each
+          const int k4 = kk & 3;
+          mma_bf16(tm + 128, sdesc_kmajor_sw128((kk < 4 ? phi : plo) + k4 * 32),
+                   sdesc_mnmajor_sw128(vs + k4 * 2048, 8192), idO, j > 0 || kk > 0);
+        }
+        mma_commit(b_odone);
+        mma_commit(b_empty + 8 * (j % TC_NS));
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax rows
+    const int rho = tid;  // 0..127 = TMEM lane
+    const int pi = rho / g, hl = rho % g;
+    const int ri = i0 + pi;
+    const bool rvalid = ri < a.n_rows && pi < pb_rows;
+    const int t = first + ri;
+    const int head = kvh * g + hl;
+    const int hi_row = rvalid ? t - r : 0;
+    // the query row: rotated at t (fp64 angles), split hi/lo, into the two K-major A tiles
+    {
+      const int64_t qb = ((int64_t)(b * a.n_rows + (rvalid ? ri : 0)) * Hq + head) * 128;
+      unsigned char* qh = sm + OFF_QHI;
+      unsigned char* ql = sm + OFF_QLO;
+      for (int c = 0; c < 16; ++c) {  // 16-byte chunk c: dims 8c .. 8c+7
+        uint32_t h4[4], l4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * c + u;  // rotation pair (2j, 2j+1)
+          float e0 = 0.f, e1 = 0.f;
+          if (rvalid) {
+            double sn, cs;
+            sincos((double)t * p.rope_freqs[j], &sn, &cs);
+            const double x0 = load_in(p.q_pre, qb + 2 * j, p.in_dtype), x1 = load_in(p.q_pre, qb + 2 * j + 1, p.in_dtype);
+            e0 = (float)(x0 * cs - x1 * sn);
+            e1 = (float)(x0 * sn + x1 * cs);
+          }
+          const float h0 = __bfloat162float(__float2bfloat16_rn(e0)), h1 = __bfloat162float(__float2bfloat16_rn(e1));
+          h4[u] = pack2(h0, h1);
+          l4[u] = pack2(e0 - h0, e1 - h1);
+        }
+        const uint32_t off = kmaj_off(rho, 8 * c, 128);
+        *reinterpret_cast<uint4*>(qh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+        *reinterpret_cast<uint4*>(ql + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(b_qfull);
+    }
+    const float scale2 = (float)(1.0 / sqrt(128.0)) * kLog2e;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int hi_mask = min(hi_row, k1);
+    float M = -CUDART_INF_F, Z = 0.f;
+    unsigned char* ph = sm + OFF_PHI;
+    unsigned char* pl = sm + OFF_PLO;
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait_parity(b_sfull + 8 * (j & 1), (j >> 1) & 1);
+      tc_fence_after();
+      float l[TC_TILE];
+      {
+        uint32_t v[32];
+        const uint32_t sa = tm + lane_base + (uint32_t)((j & 1) * TC_TILE);
+        tmem_ld32(sa, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) l[c] = __uint_as_float(v[c]);
+        tmem_ld32(sa + 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) l[32 + c] = __uint_as_float(v[c]);
+      }
+      const int kt = k0 + j * TC_TILE;
+      float mx = -CUDART_INF_F;
+#pragma unroll
+      for (int c = 0; c < TC_TILE; ++c) {
+        l[c] = (kt + c <= hi_mask) ? l[c] * scale2 : -CUDART_INF_F;
+        mx = fmaxf(mx, l[c]);
+      }
+      const float Mn = (M == -CUDART_INF_F || mx > M + 8.f) ? fmaxf(M, mx) : M;
+      const float alpha = (M == -CUDART_INF_F || Mn == M) ? 1.f : exp2f(M - Mn);
+      float zs = 0.f;
+#pragma unroll
+      for (int c = 0; c < TC_TILE; ++c) {
+        l[c] = (Mn == -CUDART_INF_F) ? 0.f : exp2f(l[c] - Mn);
+        zs += l[c];
+      }
+      Z = Z * alpha + zs;
+      if (j > 0) mbar_wait_parity(b_odone, (j - 1) & 1);  // PV(j-1) done: P free, O stable
+      tc_fence_after();
+      if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O row *= alpha (warp-collective TMEM access)
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+          tmem_ld32(tm + 128 + lane_base + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+          tmem_st32(tm + 128 + lane_base + c, v);
+        }
+        tmem_wait_st();
+      }
+      M = Mn;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // keys 8c .. 8c+7 of the tile, split hi/lo
+        uint32_t h4[4], l4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float x0 = l[8 * c + 2 * u], x1 = l[8 * c + 2 * u + 1];
+          const float h0 = __bfloat162float(__float2bfloat16_rn(x0)), h1 = __bfloat162float(__float2bfloat16_rn(x1));
+          h4[u] = pack2(h0, h1);
+          l4[u] = pack2(x0 - h0, x1 - h1);
+        }
+        const uint32_t off = kmaj_off(rho, 8 * c, 128);
+        *reinterpret_cast<uint4*>(ph + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+        *reinterpret_cast<uint4*>(pl + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(b_pfull);
+    }
+    // epilogue: this row's normalised (acc, lse), 32 TMEM columns at a time
+    if (nt > 0) {
+      mbar_wait_parity(b_odone, (nt - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = Z > 0.f ? 1.f / Z : 0.f;
+    const float lse = Z > 0.f ? M * kLn2 + logf(Z) : -CUDART_INF_F;
+    const int slot = rvalid ? (t - 1) % W : 0;
+    float* dst = nullptr;
+    if (rvalid) {
+      if (a.n_chunks == 1) {
+        dst = static_cast<float*>(p.ring_acc) + (((int64_t)b * Hq + head) * W + slot) * 128;
+        static_cast<float*>(p.ring_lse)[((int64_t)b * Hq + head) * W + slot] = lse;
+      } else {
+        dst = static_cast<float*>(a.part) + ((((int64_t)b * a.n_rows + ri) * Hq + head) * a.n_chunks + ch) * 129;
+        dst[128] = lse;
+      }
+    }
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      uint32_t v[32];
+      if (nt > 0) {
+        tmem_ld32(tm + 128 + lane_base + c, v);  // warp-collective: every lane takes part
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0u;
+      }
+      if (rvalid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 v4 = make_float4(__uint_as_float(v[e]) * inv, __uint_as_float(v[e + 1]) * inv,
+                                        __uint_as_float(v[e + 2]) * inv, __uint_as_float(v[e + 3]) * inv);
+          if (a.n_chunks == 1) *reinterpret_cast<float4*>(dst + c + e) = v4;
+          else { dst[c + e] = v4.x; dst[c + e + 1] = v4.y; dst[c + e + 2] = v4.z; dst[c + e + 3] = v4.w; }
+        }
+      }
+    }
+    if (rvalid && ch == 0) {  // the ring's query row (pre-RoPE, bf16 like the decode write-back)
+      const int64_t qb = ((int64_t)(b * a.n_rows + ri) * Hq + head) * 128;
+      __nv_bfloat16* rq = static_cast<__nv_bfloat16*>(p.ring_q) + (((int64_t)b * Hq + head) * W + slot) * 128;
+      for (int e = 0; e < 128; ++e) rq[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
+      if (p.ring_qp) {
+        __nv_bfloat16* rp =
+            static_cast<__nv_bfloat16*>(p.ring_qp) + (((int64_t)b * Hq + head) * W + slot) * MAC_PLANAR_DIMS;
+        for (int e = 0; e < MAC_PLANAR_DIMS; ++e) rp[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) tmem_dealloc(tm, 256);
+}
+
+bool ring_build_tc_supported(const MacDecodeParams& p) {
+  const int g = p.n_q_heads / p.n_kv_heads;
+  return p.storage == MAC_MODE_BF16 && p.head_dim == 128 && p.head_dim_v == 128 && g >= 1 && 128 % g == 0 &&
+         g <= 8 && p.page_size % 16 == 0 && p.kv_offset == 0 && p.kv_limit == 0 &&
+         (reinterpret_cast<uintptr_t>(p.k_cache) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.v_cache) & 15) == 0;
+}
+
+cudaError_t launch_ring_build_tc(const MacDecodeParams& p, const MacRingBuildParams& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ring_build_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mK, mV;
+  if (!encode_cache_map(&mK, p.k_cache) || !encode_cache_map(&mV, p.v_cache)) return cudaErrorInvalidValue;
+  const int g = p.n_q_heads / p.n_kv_heads;
+  const long n_pb = (a.n_rows + 128 / g - 1) / (128 / g);
+  const long items = (long)p.batch * p.n_kv_heads * n_pb * a.n_chunks;
+  if (items > 0x7fffffffL) return cudaErrorInvalidValue;
+  ring_build_tc_kernel<<<(unsigned)items, TC_THREADS, TC_SMEM, st>>>(mK, mV, p, a);
+  return cudaGetLastError();
+}
+
+}  // namespace mac

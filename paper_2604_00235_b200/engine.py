@@ -594,13 +594,14 @@ class BatchDecodeEngine:
         return (cfg.storage == "bf16" and cfg.d == 128 and cfg.d_v == 128 and 8 % g == 0
                 and self.page_size % 16 == 0 and self.kv_offset == 0 and self.kv_limit == 0)
 
-    def build_ring(self, layer: int, q_rows: torch.Tensor, n_chunks: int | None = None):
+    def build_ring(self, layer: int, q_rows: torch.Tensor, n_chunks: int | None = None, variant: str = "auto"):
         """Ring entries of the last q_rows.shape[1] stored positions of every request from the KV
         already in the cache (mac_build_ring): slot (t-1) % W <- (q_t, AS[1, t-r] under R_t q_t).
         q_rows: [B, n_rows, Hq, d] pre-RoPE queries of positions seq_len-n_rows+1 .. seq_len (a
         caller-owned pool filled by the serving system's own prefill works the same way).
         n_chunks splits each row block's keys for parallelism (default: enough CTAs for ~4
-        waves on 148 SMs)."""
+        waves on 148 SMs).  variant: "auto" (the tcgen05 kernel where it applies), "mma"
+        (mma.sync, 8-row warps) or "tcgen05" (UMMA, 128-row CTAs)."""
         cfg, B = self.cfg, self.batch
         if not self.ring_build_supported():
             raise ValueError("mac_build_ring needs the bf16 d = 128 path (see prefill)")
@@ -613,7 +614,9 @@ class BatchDecodeEngine:
             return
         q_rows = q_rows.contiguous()
         g = cfg.n_q_heads // cfg.n_kv_heads
-        blocks = B * cfg.n_kv_heads * -(-n_rows // (8 * (8 // g)))
+        vid = {"auto": 0, "mma": 1, "tcgen05": 2}[variant]
+        rows_per_cta = 8 * (8 // g) if vid == 1 else 128 // g
+        blocks = B * cfg.n_kv_heads * -(-n_rows // rows_per_cta)
         if n_chunks is None:
             longest = int(self.seq_lens[layer].max().item())
             n_chunks = max(1, min(-(-4 * SM_COUNT_B200 // blocks), -(-longest // 2048)))
@@ -622,7 +625,8 @@ class BatchDecodeEngine:
             part = torch.empty(B * n_rows * cfg.n_q_heads * n_chunks * (cfg.d_v + 1), dtype=torch.float32,
                                device=self.device)
         P = self._build_params(layer, q_rows, q_rows, q_rows, _IN_DT[q_rows.dtype], False)
-        rb = _lib.MacRingBuildParams(n_rows=n_rows, n_chunks=n_chunks, part=part.data_ptr() if part is not None else None)
+        rb = _lib.MacRingBuildParams(n_rows=n_rows, n_chunks=n_chunks, part=part.data_ptr() if part is not None else None,
+                                     variant=vid)
         # (part is freed back to the caching allocator on this stream: stream order keeps it live
         # until the merge kernel has read it)
         _lib.check(_lib.load().mac_build_ring(C.byref(P), C.byref(rb), C.c_void_p(self._stream())), "mac_build_ring")

@@ -88,11 +88,13 @@ def test_prefill_rejects_bad_shapes():
         eng.prefill(0, z, z, z)  # keys must have Hkv = 2 heads
 
 
+@pytest.mark.parametrize("variant", ["tcgen05", "mma"])
 @pytest.mark.parametrize("chunks", [1, 3])
-def test_build_ring_gemm_form_matches_decode_steps(chunks):
-    """The tensor-core ring build (mac_build_ring) against the forced-miss decode steps it
-    replaces, on the same prompt: ring queries identical, summaries within 2e-5, with one key
-    chunk and with split keys (merge kernel).  GQA 32/8 and 8/1 (g = 4, 8), a band and r = 0."""
+def test_build_ring_gemm_form_matches_decode_steps(chunks, variant):
+    """The tensor-core ring build (mac_build_ring; the tcgen05/TMEM/TMA kernel and the mma.sync
+    kernel) against the forced-miss decode steps it replaces, on the same prompt: ring queries
+    identical, summaries within 2e-5, with one key chunk and with split keys (merge kernel).
+    GQA 32/8 and 8/1 (g = 4, 8), a band and r = 0."""
     from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, SyntheticSpec, gen_synthetic
 
     for hq, hkv, n, W, r in ((32, 8, 700, 128, 32), (8, 1, 333, 64, 0)):
@@ -113,14 +115,15 @@ def test_build_ring_gemm_form_matches_decode_steps(chunks):
 
         _lib.check(_lib.load().mac_prefill_kv(P, n, a._stream()), "mac_prefill_kv")
         a._len[0] = n
-        a.build_ring(0, q[:, n - W:], n_chunks=chunks)
+        a.build_ring(0, q[:, n - W:], n_chunks=chunks, variant=variant)
         torch.cuda.synchronize()
         assert torch.equal(a.ring_q[0], s.ring_q[0])
         assert torch.equal(a.ring_qp[0], s.ring_qp[0])
         la, ls = a.ring_lse[0].double(), s.ring_lse[0].double()
         fin = torch.isfinite(ls)
         assert torch.equal(torch.isfinite(la), fin)
-        assert (la[fin] - ls[fin]).abs().max().item() <= 2e-5
+        # lse ~ 36 on this peaked workload: fp32 roundoff of differently ordered sums (relative)
+        assert ((la[fin] - ls[fin]).abs() / ls[fin].abs().clamp_min(1.0)).max().item() <= 2e-6
         ra, rs = a.ring_acc[0].double(), s.ring_acc[0].double()
         rel = (ra - rs).norm(dim=-1) / rs.norm(dim=-1).clamp_min(1e-30)
         assert rel[fin].max().item() <= 2e-5, rel[fin].max().item()

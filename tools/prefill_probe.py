@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--band", type=int, default=256)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--variant", default="auto", choices=("auto", "mma", "tcgen05"))
     a = ap.parse_args()
     import torch
 
@@ -53,7 +54,7 @@ def main():
     for _ in range(a.reps + 1):
         e0, e1 = ev(), ev()
         e0.record()
-        eng.build_ring(0, q, n_chunks=a.chunks or None)
+        eng.build_ring(0, q, n_chunks=a.chunks or None, variant=a.variant)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -78,7 +79,8 @@ def main():
     print(json.dumps({"batch": a.batch, "ctx": a.ctx, "rows_per_request": rows, "build_ring_ms": round(ms, 3),
                       "algorithmic_tflops": round(flops / ms / 1e9, 1), "issued_tflops": round(2 * flops / ms / 1e9, 1),
                       "forced_miss_step_ms": round(step_ms, 3), "step_based_ms": round(step_ms * rows, 1),
-                      "speedup_vs_steps": round(step_ms * rows / ms, 1), "n_chunks": a.chunks or "auto"}))
+                      "speedup_vs_steps": round(step_ms * rows / ms, 1), "n_chunks": a.chunks or "auto",
+                      "variant": a.variant}))
 
 
 if __name__ == "__main__":
