@@ -4,16 +4,18 @@
 // flash-attention pass with a causal lag of r, M = 128 query rows per CTA.
 //
 // CTA = (request, kv head, block of 128/g positions -> 128 rows = positions x g heads, key chunk).
-// Warp roles (192 threads):
-//   warps 0-3  one thread per row: rotate its query (fp64 angles), split it hi/lo into the two
-//              bf16 A operands; per 64-key tile read its S row from TMEM, online softmax in the
-//              log2 domain (lazy rescale: the reference max moves only by > 8), write P hi/lo
-//              (bf16) into shared memory, rescale its O row in TMEM when the max moved;
-//              epilogue O / Z and lse -> ring slot (or a chunk partial)
-//   warp 4     one elected thread issues the UMMAs: S = Q_hi K^T + Q_lo K^T (K-major A and B,
+// Warp roles (320 threads):
+//   warps 0-7  two threads per row (warp w and w+4 share TMEM lanes 32 (w % 4) ..; warp w < 4 takes
+//              columns 0-31 of each S tile and O columns 0-63, warp w+4 the rest): rotate the
+//              query (fp64 angles), pre-scale it by log2(e)/sqrt(d) and split it hi/lo into the
+//              two bf16 A operands; per 64-key tile read the S half-row from TMEM, exchange the
+//              row max with the partner warp, online softmax in the log2 domain (lazy rescale:
+//              the reference max moves only by > 8), write P hi/lo (bf16) into shared memory,
+//              rescale the O half-row in TMEM when the max moved; epilogue O / Z, lse -> ring
+//   warp 8     one elected thread issues the UMMAs: S = Q_hi K^T + Q_lo K^T (K-major A and B,
 //              M = 128, N = 64, fp32 in TMEM, double-buffered) and O += P_hi V + P_lo V (V
 //              MN-major, N = 128); tcgen05.commit signals S ready / P consumed / stage free
-//   warp 5     TMA producer: each 64-key tile is 4 pages x 2 dim halves of K and of V (2D tensor
+//   warp 9     TMA producer: each 64-key tile is 4 pages x 2 dim halves of K and of V (2D tensor
 //              maps over the paged cache, SWIZZLE_128B = the UMMA canonical layout), 3 stages
 // The hi/lo splits keep the logits and P exact to fp32 (the parity the decode kernels hold, see
 // amend_mma.cuh); each MMA pair reads the same K or V tile.  Descriptor and TMEM layouts:
@@ -30,13 +32,14 @@ bool encode_cache_map(CUtensorMap* m, const void* ptr);  // amend_tma.cu
 
 namespace {
 using namespace umma;
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 320;  // 8 softmax warps, the UMMA issuer, the TMA producer
 constexpr int TC_NS = 3;                   // K/V stages
 constexpr int TC_TILE = 64;                // keys per tile
 constexpr int OFF_QHI = 0, OFF_QLO = 32768, OFF_PHI = 65536, OFF_PLO = 81920, OFF_KV = 98304;
 constexpr int KV_STAGE = 32768;            // K 16 KB (2 atoms x 64 keys x 128 B) + V 16 KB
 constexpr int OFF_BAR = OFF_KV + TC_NS * KV_STAGE;
-constexpr int TC_SMEM = OFF_BAR + 256 + 1024;
+constexpr int OFF_RED = OFF_BAR + 256;          // [2 tiles][2 halves][128 rows] f32 row maxima, then Z
+constexpr int TC_SMEM = OFF_RED + 2 * 2 * 128 * 4 + 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -94,18 +97,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     mbar_init(b_sfull, 1);
     mbar_init(b_sfull + 8, 1);
-    mbar_init(b_pfull, 128);
+    mbar_init(b_pfull, 256);
     mbar_init(b_odone, 1);
-    mbar_init(b_qfull, 128);
+    mbar_init(b_qfull, 256);
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc(smem_u32(tmem_slot), 256);
+  if (warp == 8) tmem_alloc(smem_u32(tmem_slot), 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = *tmem_slot;  // S buffers at columns 0 / 64, O at 128
 
-  if (warp == 5) {
+  if (warp == 9) {
     // ------------------------------------------------------------------ TMA producer
     for (int j = 0; j < nt; ++j) {
       const int st = j % TC_NS;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 8) {
     // ------------------------------------------------------------------ UMMA issuer
     if (lane == 0 && nt > 0) {
       const uint32_t idS = instr_desc_bf16(128, TC_TILE, false, false);
@@ -173,19 +176,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------------ softmax rows
-    const int rho = tid;  // 0..127 = TMEM lane
+    const int half = warp >> 2;              // S columns 32 half .., O columns 64 half ..
+    const int rho = (warp & 3) * 32 + lane;  // row = TMEM lane
     const int pi = rho / g, hl = rho % g;
     const int ri = i0 + pi;
     const bool rvalid = ri < a.n_rows && pi < pb_rows;
     const int t = first + ri;
     const int head = kvh * g + hl;
     const int hi_row = rvalid ? t - r : 0;
-    // the query row: rotated at t (fp64 angles), split hi/lo, into the two K-major A tiles
+    const float scale2 = (float)(1.0 / sqrt(128.0)) * kLog2e;
+    // the query row: rotated at t (fp64 angles), scaled by log2(e)/sqrt(d) (the logits come out
+    // of the MMA in the log2 domain), split hi/lo into the two K-major A tiles; this thread writes
+    // dims 64 half .. 64 half + 63
     {
       const int64_t qb = ((int64_t)(b * a.n_rows + (rvalid ? ri : 0)) * Hq + head) * 128;
       unsigned char* qh = sm + OFF_QHI;
       unsigned char* ql = sm + OFF_QLO;
-      for (int c = 0; c < 16; ++c) {  // 16-byte chunk c: dims 8c .. 8c+7
+      for (int c = 8 * half; c < 8 * half + 8; ++c) {  // 16-byte chunk c: dims 8c .. 8c+7
         uint32_t h4[4], l4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -195,8 +202,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             double sn, cs;
             sincos((double)t * p.rope_freqs[j], &sn, &cs);
             const double x0 = load_in(p.q_pre, qb + 2 * j, p.in_dtype), x1 = load_in(p.q_pre, qb + 2 * j + 1, p.in_dtype);
-            e0 = (float)(x0 * cs - x1 * sn);
-            e1 = (float)(x0 * sn + x1 * cs);
+            e0 = (float)(x0 * cs - x1 * sn) * scale2;
+            e1 = (float)(x0 * sn + x1 * cs) * scale2;
           }
           const float h0 = __bfloat162float(__float2bfloat16_rn(e0)), h1 = __bfloat162float(__float2bfloat16_rn(e1));
           h4[u] = pack2(h0, h1);
@@ -209,61 +216,62 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       fence_proxy_async_smem();
       mbar_arrive(b_qfull);
     }
-    const float scale2 = (float)(1.0 / sqrt(128.0)) * kLog2e;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int hi_mask = min(hi_row, k1);
-    float M = -CUDART_INF_F, Z = 0.f;
+    float* red = reinterpret_cast<float*>(sm + OFF_RED);  // [tile parity][half][row]
+    const uint32_t pair_bar = 1 + (warp & 3);             // named barrier of warps w and w+4
+    float M = -CUDART_INF_F, Z = 0.f;                     // Z: this half's columns
     unsigned char* ph = sm + OFF_PHI;
     unsigned char* pl = sm + OFF_PLO;
     for (int j = 0; j < nt; ++j) {
       mbar_wait_parity(b_sfull + 8 * (j & 1), (j >> 1) & 1);
       tc_fence_after();
-      float l[TC_TILE];
+      float l[32];
       {
         uint32_t v[32];
-        const uint32_t sa = tm + lane_base + (uint32_t)((j & 1) * TC_TILE);
-        tmem_ld32(sa, v);
+        tmem_ld32(tm + lane_base + (uint32_t)((j & 1) * TC_TILE + 32 * half), v);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 32; ++c) l[c] = __uint_as_float(v[c]);
-        tmem_ld32(sa + 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 32; ++c) l[32 + c] = __uint_as_float(v[c]);
       }
-      const int kt = k0 + j * TC_TILE;
-      float mx = -CUDART_INF_F;
+      const int kt = k0 + j * TC_TILE + 32 * half;
+      if (kt + 31 > hi_mask) {  // a tile straddling this row's last key (or past it): mask
 #pragma unroll
-      for (int c = 0; c < TC_TILE; ++c) {
-        l[c] = (kt + c <= hi_mask) ? l[c] * scale2 : -CUDART_INF_F;
-        mx = fmaxf(mx, l[c]);
+        for (int c = 0; c < 32; ++c) l[c] = (kt + c <= hi_mask) ? l[c] : -CUDART_INF_F;
       }
+      float mx = l[0];
+#pragma unroll
+      for (int c = 1; c < 32; ++c) mx = fmaxf(mx, l[c]);
+      red[((j & 1) * 2 + half) * 128 + rho] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+      mx = fmaxf(mx, red[((j & 1) * 2 + (half ^ 1)) * 128 + rho]);
       const float Mn = (M == -CUDART_INF_F || mx > M + 8.f) ? fmaxf(M, mx) : M;
       const float alpha = (M == -CUDART_INF_F || Mn == M) ? 1.f : exp2f(M - Mn);
       float zs = 0.f;
 #pragma unroll
-      for (int c = 0; c < TC_TILE; ++c) {
+      for (int c = 0; c < 32; ++c) {
         l[c] = (Mn == -CUDART_INF_F) ? 0.f : exp2f(l[c] - Mn);
         zs += l[c];
       }
       Z = Z * alpha + zs;
       if (j > 0) mbar_wait_parity(b_odone, (j - 1) & 1);  // PV(j-1) done: P free, O stable
       tc_fence_after();
-      if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O row *= alpha (warp-collective TMEM access)
+      if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O half-row *= alpha (warp-collective TMEM access)
         uint32_t v[32];
 #pragma unroll
-        for (int c = 0; c < 128; c += 32) {
-          tmem_ld32(tm + 128 + lane_base + c, v);
+        for (int c = 0; c < 64; c += 32) {
+          const uint32_t oa = tm + 128 + lane_base + (uint32_t)(64 * half + c);
+          tmem_ld32(oa, v);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-          tmem_st32(tm + 128 + lane_base + c, v);
+          tmem_st32(oa, v);
         }
         tmem_wait_st();
       }
       M = Mn;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {  // keys 8c .. 8c+7 of the tile, split hi/lo
+      for (int c = 0; c < 4; ++c) {  // keys 32 half + 8c .. +7 of the tile, split hi/lo
         uint32_t h4[4], l4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           h4[u] = pack2(h0, h1);
           l4[u] = pack2(x0 - h0, x1 - h1);
         }
-        const uint32_t off = kmaj_off(rho, 8 * c, 128);
+        const uint32_t off = kmaj_off(rho, 32 * half + 8 * c, 128);
         *reinterpret_cast<uint4*>(ph + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
         *reinterpret_cast<uint4*>(pl + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
       }
@@ -280,26 +288,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       mbar_arrive(b_pfull);
     }
-    // epilogue: this row's normalised (acc, lse), 32 TMEM columns at a time
+    // epilogue: the row's Z from both halves, this half's 64 normalised acc columns, the lse
+    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // both halves past their last red read
+    red[(2 + half) * 128 + rho] = Z;
+    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+    const float Zt = Z + red[(2 + (half ^ 1)) * 128 + rho];
     if (nt > 0) {
       mbar_wait_parity(b_odone, (nt - 1) & 1);
       tc_fence_after();
     }
-    const float inv = Z > 0.f ? 1.f / Z : 0.f;
-    const float lse = Z > 0.f ? M * kLn2 + logf(Z) : -CUDART_INF_F;
+    const float inv = Zt > 0.f ? 1.f / Zt : 0.f;
+    const float lse = Zt > 0.f ? M * kLn2 + logf(Zt) : -CUDART_INF_F;
     const int slot = rvalid ? (t - 1) % W : 0;
     float* dst = nullptr;
     if (rvalid) {
       if (a.n_chunks == 1) {
         dst = static_cast<float*>(p.ring_acc) + (((int64_t)b * Hq + head) * W + slot) * 128;
-        static_cast<float*>(p.ring_lse)[((int64_t)b * Hq + head) * W + slot] = lse;
+        if (half == 0) static_cast<float*>(p.ring_lse)[((int64_t)b * Hq + head) * W + slot] = lse;
       } else {
         dst = static_cast<float*>(a.part) + ((((int64_t)b * a.n_rows + ri) * Hq + head) * a.n_chunks + ch) * 129;
-        dst[128] = lse;
+        if (half == 0) dst[128] = lse;
       }
     }
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 32) {
+    for (int c = 64 * half; c < 64 * half + 64; c += 32) {
       uint32_t v[32];
       if (nt > 0) {
         tmem_ld32(tm + 128 + lane_base + c, v);  // warp-collective: every lane takes part
@@ -318,11 +330,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    if (rvalid && ch == 0) {  // the ring's query row (pre-RoPE, bf16 like the decode write-back)
+    if (rvalid && ch == 0) {  // the ring's query row (pre-RoPE, bf16 like the decode write-back), 64 dims each
       const int64_t qb = ((int64_t)(b * a.n_rows + ri) * Hq + head) * 128;
       __nv_bfloat16* rq = static_cast<__nv_bfloat16*>(p.ring_q) + (((int64_t)b * Hq + head) * W + slot) * 128;
-      for (int e = 0; e < 128; ++e) rq[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
-      if (p.ring_qp) {
+      for (int e = 64 * half; e < 64 * half + 64; ++e) rq[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
+      if (p.ring_qp && half == 0) {
         __nv_bfloat16* rp =
             static_cast<__nv_bfloat16*>(p.ring_qp) + (((int64_t)b * Hq + head) * W + slot) * MAC_PLANAR_DIMS;
         for (int e = 0; e < MAC_PLANAR_DIMS; ++e) rp[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) tmem_dealloc(tm, 256);
+  if (warp == 8) tmem_dealloc(tm, 256);
 }
 
 bool ring_build_tc_supported(const MacDecodeParams& p) {
