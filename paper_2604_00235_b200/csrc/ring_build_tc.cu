@@ -276,9 +276,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float x0 = l[8 * c + 2 * u], x1 = l[8 * c + 2 * u + 1];
-          const float h0 = __bfloat162float(__float2bfloat16_rn(x0)), h1 = __bfloat162float(__float2bfloat16_rn(x1));
-          h4[u] = pack2(h0, h1);
-          l4[u] = pack2(x0 - h0, x1 - h1);
+          h4[u] = pack2(x0, x1);  // one packed convert; the hi halves back as floats by bit shifts
+          l4[u] = pack2(x0 - __uint_as_float(h4[u] << 16), x1 - __uint_as_float(h4[u] & 0xffff0000u));
         }
         const uint32_t off = kmaj_off(rho, 32 * half + 8 * c, 128);
         *reinterpret_cast<uint4*>(ph + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
