@@ -239,19 +239,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c) l[c] = (kt + c <= hi_mask) ? l[c] : -CUDART_INF_F;
       }
-      float mx = l[0];
+      float mx;
+      {  // tree reduction: 5 dependent levels instead of a 31-long chain
+        float m16[16];
 #pragma unroll
-      for (int c = 1; c < 32; ++c) mx = fmaxf(mx, l[c]);
+        for (int c = 0; c < 16; ++c) m16[c] = fmaxf(l[c], l[c + 16]);
+#pragma unroll
+        for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+          for (int c = 0; c < w; ++c) m16[c] = fmaxf(m16[c], m16[c + w]);
+        mx = m16[0];
+      }
       red[((j & 1) * 2 + half) * 128 + rho] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
       mx = fmaxf(mx, red[((j & 1) * 2 + (half ^ 1)) * 128 + rho]);
       const float Mn = (M == -CUDART_INF_F || mx > M + 8.f) ? fmaxf(M, mx) : M;
       const float alpha = (M == -CUDART_INF_F || Mn == M) ? 1.f : exp2f(M - Mn);
-      float zs = 0.f;
+      float zs;
+      {
+        const float nm = (Mn == -CUDART_INF_F) ? 0.f : -Mn;  // a fully masked row: exp2(-inf) = 0
+        float z8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        l[c] = (Mn == -CUDART_INF_F) ? 0.f : exp2f(l[c] - Mn);
-        zs += l[c];
+        for (int c = 0; c < 32; ++c) {
+          l[c] = exp2f(l[c] + nm);
+          z8[c & 7] += l[c];
+        }
+        zs = ((z8[0] + z8[1]) + (z8[2] + z8[3])) + ((z8[4] + z8[5]) + (z8[6] + z8[7]));
       }
       Z = Z * alpha + zs;
       if (j > 0) mbar_wait_parity(b_odone, (j - 1) & 1);  // PV(j-1) done: P free, O stable
