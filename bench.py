@@ -72,9 +72,9 @@ def l2_flush(buf: torch.Tensor):
 
 def ncu_traffic(stage: str):
     """Per-launch DRAM bytes (read + write) of a stage's kernel from the committed ncu --set full
-    capture (profiles/r01/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    capture (profiles/r02/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")) as fh:
             return float(json.load(fh)[stage]["traffic_bytes"])
     except Exception:
         return None
@@ -600,7 +600,7 @@ def run_ours(args, wl):
             "roofline": {"bound": "hbm", "achieved": kern[dom]["gbs"], "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": ncu_traffic(dom),
                          "algorithmic_bytes": kern[dom]["bytes"], "kernel": dom,
-                         "traffic_source": "profiles/r01/ncu_traffic.json (ncu --set full, DRAM read+write per launch)"},
+                         "traffic_source": "profiles/r02/ncu_traffic.json (ncu --set full, DRAM read+write per launch)"},
             "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "StepGraph replay: pinned-host q/k/v pulled over PCIe by mac_io_copy (zero-copy kernel), the step kernels, the complete kernel writing the bf16 output into the pinned host buffer (out_bf16)",

@@ -638,8 +638,9 @@ class BatchDecodeEngine:
         return int(_lib.load().mac_match_path(P))
 
     # miss fraction above which the adaptive engine takes the one-pass scan even where the dense
-    # kernel is available (profiles/r02/SUMMARY.md, "Miss regime")
-    DENSE_MAX_MISS = 0.5
+    # kernel is available (C3 geometry at 16K: 30 % misses 371 us dense vs 315 us one-pass;
+    # 10 %: 188 vs 203 us; profiles/r02/miss_sweep_max_chunks.jsonl, bench c3mix)
+    DENSE_MAX_MISS = 0.2
 
     def _choose_match_mode(self):
         """The step's match scan (MacDecodeParams.match_mode), fixed for all of its stages:

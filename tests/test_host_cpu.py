@@ -205,17 +205,17 @@ def test_io_entry_points_validate_without_gpu():
 
 
 def test_ncu_traffic_summary_matches_committed_capture():
-    """profiles/r01/ncu_traffic.json (the bench's roofline.traffic) is what tools/ncu_traffic.py
+    """profiles/r02/ncu_traffic.json (the bench's roofline.traffic) is what tools/ncu_traffic.py
     derives from the committed ncu capture of the decode step."""
     import json
     import subprocess
     import sys
 
     res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_traffic.py"),
-                          os.path.join(ROOT, "profiles", "r01", "ncu_kernels.csv")],
+                          os.path.join(ROOT, "profiles", "r02", "ncu_kernels_c3.csv")],
                          capture_output=True, text=True, check=True)
     got = json.loads(res.stdout)
-    with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as fh:
+    with open(os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")) as fh:
         want = json.load(fh)
     for stage in ("mac_match_scan", "mac_match_verify", "mac_amend", "mac_complete"):
         assert got[stage]["traffic_bytes"] == want[stage]["traffic_bytes"], stage
