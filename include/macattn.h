@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 11
+#define MACATTN_ABI_VERSION 12
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -165,6 +165,11 @@ typedef struct MacDecodeParams {
                                  {heads that missed, heads} over the steps since the last
                                  publication, stored at the start of every 8th step (the complete
                                  kernel counts, the append warps publish) */
+  int32_t inputs_host;        /* 1: q_pre / k_pre / v_in are device aliases of pinned host memory
+                                 (zero-copy).  On the two-pass bf16 d = 128 path the step reads
+                                 them over the host link once: the scan its 16 query dims, the
+                                 append warps the rest, staging q in the workspace for the later
+                                 kernels — no separate input copy before the step */
 } MacDecodeParams;
 
 /* Per-shard (acc, lse) partial merge for the KV-sharded miss path. */

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 11
+ABI_VERSION = 12
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -118,6 +118,7 @@ class MacDecodeParams(C.Structure):
         ("workspace_bytes", C.c_size_t),
         ("match_mode", C.c_int32),
         ("feedback", C.c_void_p),
+        ("inputs_host", C.c_int32),
     ]
 
 

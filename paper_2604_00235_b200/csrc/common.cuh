@@ -64,6 +64,13 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f64<__nv_bfloat16>(dou
   return __float2bfloat16_rn(__double2float_rn(x));
 }
 
+// element store into a buffer of runtime dtype (the staged inputs, inputs_host)
+__device__ __forceinline__ void store_in(void* p, int64_t i, double v, int dt) {
+  if (dt == MAC_DT_F32) static_cast<float*>(p)[i] = (float)v;
+  else if (dt == MAC_DT_BF16) static_cast<__nv_bfloat16*>(p)[i] = __double2bfloat16(v);
+  else static_cast<double*>(p)[i] = v;
+}
+
 // element load from an input tensor of runtime dtype (MAC_DT_*)
 __device__ __forceinline__ double load_in(const void* p, int64_t i, int dt) {
   if (dt == MAC_DT_F32) return (double)static_cast<const float*>(p)[i];
@@ -282,6 +289,7 @@ struct Workspace {
   size_t dstate_off; // [B*Hq] int4   two-pass match, dense heads deferred to dense_kernel (match_mode 2):
                      //               {bound D* (fp32 bits), candidate slot 1, candidate slot 2, -}
   size_t dlist_off;  // [B*Hq] i32    the deferred heads (bh), ctr[8] of them (reset by complete)
+  size_t qstage_off; // [B*Hq*d] in_dtype  the step's queries staged from host memory (inputs_host)
   size_t tl_off;     // [kTlSlots][2] u64 timeline stamps (MAC_TIMELINE builds only)
   size_t total;
 };
@@ -306,7 +314,8 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
   w.wsum_off = align256(w.hpart_off + 4 * rows * (size_t)p.window);
   w.dstate_off = align256(w.wsum_off + 16 * rows * (size_t)kMaxWsum);
   w.dlist_off = align256(w.dstate_off + 16 * rows);
-  w.tl_off = align256(w.dlist_off + 4 * rows);
+  w.qstage_off = align256(w.dlist_off + 4 * rows);
+  w.tl_off = align256(w.qstage_off + 8 * rows * (size_t)p.head_dim);
 #ifdef MAC_TIMELINE
   w.total = align256(w.tl_off + 16 * kTlSlots);
 #else
@@ -317,6 +326,11 @@ __host__ __device__ __forceinline__ Workspace workspace_layout(const MacDecodePa
 
 template <typename T> __host__ __device__ __forceinline__ T* ws_ptr(const MacDecodeParams& p, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(p.workspace) + off);
+}
+// the step's queries as the kernels after the front read them: staged in the workspace by the
+// append warps when the inputs live in host memory (inputs_host), else the caller's q_pre
+__device__ __forceinline__ const void* q_src(const MacDecodeParams& p) {
+  return p.inputs_host ? static_cast<const void*>(ws_ptr<const char>(p, workspace_layout(p).qstage_off)) : p.q_pre;
 }
 
 // development timeline (MAC_TIMELINE builds): per slot, the earliest and latest

@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(128) complete_bf16_kernel(MacDecodeParams p) {
     int lo_g = lane < g ? __ldcg(plan_lo + b * p.n_q_heads + kvh * g + lane) : (1 << 30);
     double qv[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) qv[k] = load_in(p.q_pre, (int64_t)bh * 128 + lane + 32 * k, p.in_dtype);
+    const void* qs = q_src(p);
+    for (int k = 0; k < 4; ++k) qv[k] = load_in(qs, (int64_t)bh * 128 + lane + 32 * k, p.in_dtype);
     lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, 1));
     lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, 2));
     lo_g = min(lo_g, __shfl_xor_sync(0xffffffffu, lo_g, 4));

@@ -42,6 +42,7 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
   __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(p.k_cache);
   __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(p.v_cache);
   float* qrot = ws_ptr<float>(p, w.qrot_off);
+  void* qstage = ws_ptr<void>(p, w.qstage_off);
   // bf16 / f32 inputs (exact in fp32 registers): each head's query pair used to be loaded after
   // the previous head's store — a memory round trip per head, which made the append warps, not
   // the scan, end the front kernel (C2: the verify waited 6.7 us past the last scan CTA)
@@ -72,6 +73,10 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
           const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
           const double x0 = xa[t], x1 = xb[t];
           reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+          if (p.inputs_host) {  // host-resident inputs: stage the raw query for the later kernels
+            store_in(qstage, qi, x0, p.in_dtype);
+            store_in(qstage, qi + 1, x1, p.in_dtype);
+          }
         }
       }
     } else {
@@ -79,6 +84,10 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
         const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
         const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
         reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
+        if (p.inputs_host) {
+          store_in(qstage, qi, x0, p.in_dtype);
+          store_in(qstage, qi + 1, x1, p.in_dtype);
+        }
       }
     }
   }

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   float qh[8];  // the query dims of this lane's chunk (kQDims + 8 ci ..)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    qh[i] = cload ? (float)load_in(p.q_pre, (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
+    qh[i] = cload ? (float)load_in(q_src(p), (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
   const int m = p.seq_lens[b] + 1;
   TL_MARK_DEP(p, TL_V_M, m);
   auto rest = [&](int slot) -> float {  // sum over the remaining dims of row `slot`, this row group
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, i
     float qh[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      qh[i] = cload ? (float)load_in(p.q_pre, (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
+      qh[i] = cload ? (float)load_in(q_src(p), (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
     unsigned long long key = 0ull;
     const int r0 = chunk * kDenseRows, r1 = min(W, r0 + kDenseRows);
 #pragma unroll 1

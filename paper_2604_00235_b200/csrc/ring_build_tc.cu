@@ -1,25 +1,27 @@
 // Prefill ring construction on the 5th-generation tensor cores (tcgen05 / TMEM / TMA): the same
 // contract as ring_build.cu (the ring entries of the last n positions of a cached prompt,
 // slot (t-1) mod W <- (q_t, AS[1, t-r] under R_t q_t); engine.py:374-402, 484-499) computed as a
-// flash-attention pass with a causal lag of r, M = 128 query rows per CTA.
+// flash-attention pass with a causal lag of r.
 //
-// CTA = (request, kv head, block of 128/g positions -> 128 rows = positions x g heads, key chunk).
-// Warp roles (320 threads):
-//   warps 0-7  two threads per row (warp w and w+4 share TMEM lanes 32 (w % 4) ..; warp w < 4 takes
-//              columns 0-31 of each S tile and O columns 0-63, warp w+4 the rest): rotate the
-//              query (fp64 angles), pre-scale it by log2(e)/sqrt(d) and split it hi/lo into the
-//              two bf16 A operands; per 64-key tile read the S half-row from TMEM, exchange the
-//              row max with the partner warp, online softmax in the log2 domain (lazy rescale:
-//              the reference max moves only by > 8), write P hi/lo (bf16) into shared memory,
-//              rescale the O half-row in TMEM when the max moved; epilogue O / Z, lse -> ring
-//   warp 8     one elected thread issues the UMMAs: S = Q_hi K^T + Q_lo K^T (K-major A and B,
-//              M = 128, N = 64, fp32 in TMEM, double-buffered) and O += P_hi V + P_lo V (V
-//              MN-major, N = 128); tcgen05.commit signals S ready / P consumed / stage free
+// CTA = (request, kv head, block of 256/g positions -> two 128-row query tiles of positions x g
+// heads, key chunk).  The two tiles share every K/V tile and ping-pong on the tensor core: while
+// one tile's softmax runs, the other tile's MMAs do.  Warp roles (320 threads):
+//   warps 0-3 / 4-7  tile 0 / tile 1, one thread per row (TMEM lane 32 (w % 4) + lane): rotate
+//              the query (fp64 angles), pre-scale it by log2(e)/sqrt(d), split it hi/lo into the
+//              tile's two bf16 A operands (shared memory); per 64-key tile read the S row from
+//              TMEM, online softmax in the log2 domain (lazy rescale: the reference max moves
+//              only by > 8; O is then rescaled in TMEM), write P hi/lo as packed bf16 into the
+//              same TMEM columns the S row came from; epilogue O / Z and lse -> ring slot
+//   warp 8     one elected thread issues the UMMAs: S_t = Q_hi K^T + Q_lo K^T (A and B K-major
+//              in shared memory, M = 128, N = 64, double-buffered per tile) and
+//              O_t += P_hi V + P_lo V (A = P from TMEM, B = V MN-major in shared memory, N = 128);
+//              tcgen05.commit signals S ready / O updated / K/V stage free
 //   warp 9     TMA producer: each 64-key tile is 4 pages x 2 dim halves of K and of V (2D tensor
 //              maps over the paged cache, SWIZZLE_128B = the UMMA canonical layout), 3 stages
+// TMEM per tile: S/P buffers at columns 256 t + {0, 64}, O at 256 t + 128 (all 512 columns).
 // The hi/lo splits keep the logits and P exact to fp32 (the parity the decode kernels hold, see
-// amend_mma.cuh); each MMA pair reads the same K or V tile.  Descriptor and TMEM layouts:
-// umma.cuh, validated against a host GEMM by tools/umma_probe.cu.
+// amend_mma.cuh).  Descriptor and TMEM layouts: umma.cuh, validated against a host GEMM by
+// tools/umma_probe.cu (including the TMEM A operand).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,14 +34,14 @@ bool encode_cache_map(CUtensorMap* m, const void* ptr);  // amend_tma.cu
 
 namespace {
 using namespace umma;
-constexpr int TC_THREADS = 320;  // 8 softmax warps, the UMMA issuer, the TMA producer
+constexpr int TC_THREADS = 320;            // 8 softmax warps (two tiles), the UMMA issuer, the TMA producer
 constexpr int TC_NS = 3;                   // K/V stages
 constexpr int TC_TILE = 64;                // keys per tile
-constexpr int OFF_QHI = 0, OFF_QLO = 32768, OFF_PHI = 65536, OFF_PLO = 81920, OFF_KV = 98304;
+constexpr int Q_TILE = 65536;              // one query tile: hi 32 KB + lo 32 KB (2 atoms x 128 rows x 128 B each)
+constexpr int OFF_Q = 0, OFF_KV = 2 * Q_TILE;
 constexpr int KV_STAGE = 32768;            // K 16 KB (2 atoms x 64 keys x 128 B) + V 16 KB
 constexpr int OFF_BAR = OFF_KV + TC_NS * KV_STAGE;
-constexpr int OFF_RED = OFF_BAR + 256;          // [2 tiles][2 halves][128 rows] f32 row maxima, then Z
-constexpr int TC_SMEM = OFF_RED + 2 * 2 * 128 * 4 + 1024;
+constexpr int TC_SMEM = OFF_BAR + 256 + 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   unsigned char* sm = smem_raw + (base - raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Hkv = p.n_kv_heads, Hq = p.n_q_heads, g = Hq / Hkv, r = p.band, ps = p.page_size, W = p.window;
-  const int pb_rows = 128 / g;
+  const int pb_rows = 256 / g;  // positions per CTA (two tiles of 128 / g)
   const int n_pb = (a.n_rows + pb_rows - 1) / pb_rows;
   int item = blockIdx.x;
   const int ch = item % a.n_chunks;
@@ -87,33 +89,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int k0 = 1 + tile0 * TC_TILE, k1 = min(kmax, (tile0 + per) * TC_TILE);
 
   const uint32_t bar = base + OFF_BAR;
-  const uint32_t b_full = bar, b_empty = bar + 8 * TC_NS, b_sfull = bar + 16 * TC_NS, b_pfull = b_sfull + 16,
-                 b_odone = b_pfull + 8, b_qfull = b_odone + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_BAR + 128);
+  // full[NS] empty[NS] sfull[2 tiles][2 bufs] odone[2] pfull[2] qfull[2]
+  const uint32_t b_full = bar, b_empty = bar + 8 * TC_NS, b_sfull = bar + 16 * TC_NS, b_odone = b_sfull + 32,
+                 b_pfull = b_odone + 16, b_qfull = b_pfull + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_BAR + 160);
   if (tid == 0) {
     for (int i = 0; i < TC_NS; ++i) {
       mbar_init(b_full + 8 * i, 1);
       mbar_init(b_empty + 8 * i, 1);
     }
-    mbar_init(b_sfull, 1);
-    mbar_init(b_sfull + 8, 1);
-    mbar_init(b_pfull, 256);
-    mbar_init(b_odone, 1);
-    mbar_init(b_qfull, 256);
+    for (int i = 0; i < 4; ++i) mbar_init(b_sfull + 8 * i, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(b_odone + 8 * t, 1);
+      mbar_init(b_pfull + 8 * t, 128);
+      mbar_init(b_qfull + 8 * t, 128);
+    }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc(smem_u32(tmem_slot), 256);
+  if (warp == 8) tmem_alloc(smem_u32(tmem_slot), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tm = *tmem_slot;  // S buffers at columns 0 / 64, O at 128
+  const uint32_t tm = *tmem_slot;
 
   if (warp == 9) {
     // ------------------------------------------------------------------ TMA producer
     for (int j = 0; j < nt; ++j) {
       const int st = j % TC_NS;
-      // lane s < 4: the cache row of sub-tile s (16 keys inside one page)
-      int row = 0;
+      int row = 0;  // lane s < 4: the cache row of sub-tile s (16 keys inside one page)
       if (lane < 4) {
         const int tok = k0 + j * TC_TILE + lane * 16;
         const int pg = p.page_table[(int64_t)b * p.pages_per_seq + min((tok - 1) / ps, p.pages_per_seq - 1)];
@@ -141,58 +144,64 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0 && nt > 0) {
       const uint32_t idS = instr_desc_bf16(128, TC_TILE, false, false);
       const uint32_t idO = instr_desc_bf16(128, 128, false, true);
-      const uint32_t qhi = base + OFF_QHI, qlo = base + OFF_QLO, phi = base + OFF_PHI, plo = base + OFF_PLO;
-      auto issue_s = [&](int j) {
-        const int st = j % TC_NS;
-        mbar_wait_parity(b_full + 8 * st, (j / TC_NS) & 1);
-        tc_fence_after();
-        const uint32_t ks = base + OFF_KV + st * KV_STAGE;
-        const uint32_t d = tm + (uint32_t)((j & 1) * TC_TILE);
+      auto issue_s = [&](int t, int j) {  // S_t(j) into buffer j % 2 of tile t
+        const uint32_t qhi = base + OFF_Q + t * Q_TILE, qlo = qhi + 32768;
+        const uint32_t ks = base + OFF_KV + (j % TC_NS) * KV_STAGE;
+        const uint32_t d = tm + (uint32_t)(256 * t + (j & 1) * TC_TILE);
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {  // 8 k-steps of the hi operand, then 8 of the lo operand
           const int ks8 = kk & 7;
           const uint32_t aoff = (ks8 >> 2) * 16384 + (ks8 & 3) * 32, boff = (ks8 >> 2) * 8192 + (ks8 & 3) * 32;
           mma_bf16(d, sdesc_kmajor_sw128((kk < 8 ? qhi : qlo) + aoff), sdesc_kmajor_sw128(ks + boff), idS, kk > 0);
         }
-        mma_commit(b_sfull + 8 * (j & 1));
+        mma_commit(b_sfull + 8 * (2 * t + (j & 1)));
       };
-      mbar_wait_parity(b_qfull, 0);
-      tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < nt; ++j) {
-        if (j + 1 < nt) issue_s(j + 1);
-        mbar_wait_parity(b_pfull, j & 1);
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) . V(j), P hi/lo from TMEM buffer j % 2
+        mbar_wait_parity(b_pfull + 8 * t, j & 1);
         tc_fence_after();
         const uint32_t vs = base + OFF_KV + (j % TC_NS) * KV_STAGE + 16384;
+        const uint32_t pa = tm + (uint32_t)(256 * t + (j & 1) * TC_TILE);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // P_hi . V then P_lo . V, 4 k-steps of 16 keys each
+        for (int kk = 0; kk < 8; ++kk) {  // P_hi (columns 0..31) then P_lo (32..63), 8 columns per 16 keys
           const int k4 = kk & 3;
-          mma_bf16(tm + 128, sdesc_kmajor_sw128((kk < 4 ? phi : plo) + k4 * 32),
-                   sdesc_mnmajor_sw128(vs + k4 * 2048, 8192), idO, j > 0 || kk > 0);
+          mma_bf16_ta(tm + (uint32_t)(256 * t + 128), pa + (uint32_t)((kk >> 2) * 32 + k4 * 8),
+                      sdesc_mnmajor_sw128(vs + k4 * 2048, 8192), idO, j > 0 || kk > 0);
         }
-        mma_commit(b_odone);
-        mma_commit(b_empty + 8 * (j % TC_NS));
+        mma_commit(b_odone + 8 * t);
+      };
+      mbar_wait_parity(b_qfull, 0);
+      mbar_wait_parity(b_qfull + 8, 0);
+      tc_fence_after();
+      for (int j = 0; j <= nt; ++j) {
+        if (j < nt) {
+          mbar_wait_parity(b_full + 8 * (j % TC_NS), (j / TC_NS) & 1);
+          tc_fence_after();
+          issue_s(0, j);
+          issue_s(1, j);
+        }
+        if (j > 0) {
+          issue_pv(0, j - 1);
+          issue_pv(1, j - 1);
+          mma_commit(b_empty + 8 * ((j - 1) % TC_NS));
+        }
       }
     }
   } else {
     // ------------------------------------------------------------------ softmax rows
-    const int half = warp >> 2;              // S columns 32 half .., O columns 64 half ..
-    const int rho = (warp & 3) * 32 + lane;  // row = TMEM lane
-    const int pi = rho / g, hl = rho % g;
+    const int t = warp >> 2;                 // query tile
+    const int rho = (warp & 3) * 32 + lane;  // row of the tile = TMEM lane
+    const int pi = t * (128 / g) + rho / g, hl = rho % g;
     const int ri = i0 + pi;
-    const bool rvalid = ri < a.n_rows && pi < pb_rows;
-    const int t = first + ri;
+    const bool rvalid = ri < a.n_rows;
+    const int pos = first + ri;
     const int head = kvh * g + hl;
-    const int hi_row = rvalid ? t - r : 0;
+    const int hi_row = rvalid ? pos - r : 0;
     const float scale2 = (float)(1.0 / sqrt(128.0)) * kLog2e;
-    // the query row: rotated at t (fp64 angles), scaled by log2(e)/sqrt(d) (the logits come out
-    // of the MMA in the log2 domain), split hi/lo into the two K-major A tiles; this thread writes
-    // dims 64 half .. 64 half + 63
-    {
+    {  // the query row: rotated at pos (fp64 angles), scaled into the log2 domain, split hi/lo
       const int64_t qb = ((int64_t)(b * a.n_rows + (rvalid ? ri : 0)) * Hq + head) * 128;
-      unsigned char* qh = sm + OFF_QHI;
-      unsigned char* ql = sm + OFF_QLO;
-      for (int c = 8 * half; c < 8 * half + 8; ++c) {  // 16-byte chunk c: dims 8c .. 8c+7
+      unsigned char* qh = sm + OFF_Q + t * Q_TILE;
+      unsigned char* ql = qh + 32768;
+      for (int c = 0; c < 16; ++c) {  // 16-byte chunk c: dims 8c .. 8c+7
         uint32_t h4[4], l4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -200,59 +209,62 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           float e0 = 0.f, e1 = 0.f;
           if (rvalid) {
             double sn, cs;
-            sincos((double)t * p.rope_freqs[j], &sn, &cs);
+            sincos((double)pos * p.rope_freqs[j], &sn, &cs);
             const double x0 = load_in(p.q_pre, qb + 2 * j, p.in_dtype), x1 = load_in(p.q_pre, qb + 2 * j + 1, p.in_dtype);
             e0 = (float)(x0 * cs - x1 * sn) * scale2;
             e1 = (float)(x0 * sn + x1 * cs) * scale2;
           }
-          const float h0 = __bfloat162float(__float2bfloat16_rn(e0)), h1 = __bfloat162float(__float2bfloat16_rn(e1));
-          h4[u] = pack2(h0, h1);
-          l4[u] = pack2(e0 - h0, e1 - h1);
+          h4[u] = pack2(e0, e1);
+          l4[u] = pack2(e0 - __uint_as_float(h4[u] << 16), e1 - __uint_as_float(h4[u] & 0xffff0000u));
         }
         const uint32_t off = kmaj_off(rho, 8 * c, 128);
         *reinterpret_cast<uint4*>(qh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
         *reinterpret_cast<uint4*>(ql + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
       }
       fence_proxy_async_smem();
-      mbar_arrive(b_qfull);
+      mbar_arrive(b_qfull + 8 * t);
     }
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tcol = (uint32_t)(256 * t);
     const int hi_mask = min(hi_row, k1);
-    float* red = reinterpret_cast<float*>(sm + OFF_RED);  // [tile parity][half][row]
-    const uint32_t pair_bar = 1 + (warp & 3);             // named barrier of warps w and w+4
-    float M = -CUDART_INF_F, Z = 0.f;                     // Z: this half's columns
-    unsigned char* ph = sm + OFF_PHI;
-    unsigned char* pl = sm + OFF_PLO;
-    for (int j = 0; j < nt; ++j) {
-      mbar_wait_parity(b_sfull + 8 * (j & 1), (j >> 1) & 1);
+    float M = -CUDART_INF_F, Z = 0.f;
+    int odone_seen = 0;  // O-update phases of this tile waited for (in order: parity waits stay exact)
+    auto wait_odone = [&](int upto) {  // PV_t(0 .. upto-1) complete
+      for (; odone_seen < upto; ++odone_seen) mbar_wait_parity(b_odone + 8 * t, odone_seen & 1);
       tc_fence_after();
-      float l[32];
+    };
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait_parity(b_sfull + 8 * (2 * t + (j & 1)), (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sa = tm + lane_base + tcol + (uint32_t)((j & 1) * TC_TILE);
+      float l[64];
       {
         uint32_t v[32];
-        tmem_ld32(tm + lane_base + (uint32_t)((j & 1) * TC_TILE + 32 * half), v);
+        tmem_ld32(sa, v);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 32; ++c) l[c] = __uint_as_float(v[c]);
-      }
-      const int kt = k0 + j * TC_TILE + 32 * half;
-      if (kt + 31 > hi_mask) {  // a tile straddling this row's last key (or past it): mask
+        tmem_ld32(sa + 32, v);
+        tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) l[c] = (kt + c <= hi_mask) ? l[c] : -CUDART_INF_F;
+        for (int c = 0; c < 32; ++c) l[32 + c] = __uint_as_float(v[c]);
+      }
+      const int kt = k0 + j * TC_TILE;
+      if (kt + TC_TILE - 1 > hi_mask) {  // a tile reaching past this row's last key: mask
+#pragma unroll
+        for (int c = 0; c < 64; ++c) l[c] = (kt + c <= hi_mask) ? l[c] : -CUDART_INF_F;
       }
       float mx;
-      {  // tree reduction: 5 dependent levels instead of a 31-long chain
-        float m16[16];
+      {
+        float m32[32];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) m16[c] = fmaxf(l[c], l[c + 16]);
+        for (int c = 0; c < 32; ++c) m32[c] = fmaxf(l[c], l[c + 32]);
 #pragma unroll
-        for (int w = 8; w > 0; w >>= 1)
+        for (int w = 16; w > 0; w >>= 1)
 #pragma unroll
-          for (int c = 0; c < w; ++c) m16[c] = fmaxf(m16[c], m16[c + w]);
-        mx = m16[0];
+          for (int c = 0; c < w; ++c) m32[c] = fmaxf(m32[c], m32[c + w]);
+        mx = m32[0];
       }
-      red[((j & 1) * 2 + half) * 128 + rho] = mx;
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-      mx = fmaxf(mx, red[((j & 1) * 2 + (half ^ 1)) * 128 + rho]);
       const float Mn = (M == -CUDART_INF_F || mx > M + 8.f) ? fmaxf(M, mx) : M;
       const float alpha = (M == -CUDART_INF_F || Mn == M) ? 1.f : exp2f(M - Mn);
       float zs;
@@ -260,73 +272,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const float nm = (Mn == -CUDART_INF_F) ? 0.f : -Mn;  // a fully masked row: exp2(-inf) = 0
         float z8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 64; ++c) {
           l[c] = exp2f(l[c] + nm);
           z8[c & 7] += l[c];
         }
         zs = ((z8[0] + z8[1]) + (z8[2] + z8[3])) + ((z8[4] + z8[5]) + (z8[6] + z8[7]));
       }
       Z = Z * alpha + zs;
-      if (j > 0) mbar_wait_parity(b_odone, (j - 1) & 1);  // PV(j-1) done: P free, O stable
-      tc_fence_after();
-      if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O half-row *= alpha (warp-collective TMEM access)
+      if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O row *= alpha once PV(j-1) has landed
+        wait_odone(j);
         uint32_t v[32];
 #pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          const uint32_t oa = tm + 128 + lane_base + (uint32_t)(64 * half + c);
+        for (int c = 0; c < 128; c += 32) {
+          const uint32_t oa = tm + lane_base + tcol + 128 + c;
           tmem_ld32(oa, v);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
           tmem_st32(oa, v);
         }
-        tmem_wait_st();
       }
       M = Mn;
+      {  // P hi (columns 0..31) and lo (32..63), two bf16 per column, over the S row just read
+        uint32_t ph[32], pl[32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // keys 32 half + 8c .. +7 of the tile, split hi/lo
-        uint32_t h4[4], l4[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float x0 = l[8 * c + 2 * u], x1 = l[8 * c + 2 * u + 1];
-          h4[u] = pack2(x0, x1);  // one packed convert; the hi halves back as floats by bit shifts
-          l4[u] = pack2(x0 - __uint_as_float(h4[u] << 16), x1 - __uint_as_float(h4[u] & 0xffff0000u));
+        for (int c = 0; c < 32; ++c) {
+          const float x0 = l[2 * c], x1 = l[2 * c + 1];
+          ph[c] = pack2(x0, x1);
+          pl[c] = pack2(x0 - __uint_as_float(ph[c] << 16), x1 - __uint_as_float(ph[c] & 0xffff0000u));
         }
-        const uint32_t off = kmaj_off(rho, 32 * half + 8 * c, 128);
-        *reinterpret_cast<uint4*>(ph + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
-        *reinterpret_cast<uint4*>(pl + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+        tmem_st32(sa, ph);
+        tmem_st32(sa + 32, pl);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();
+      // P(j) may be published only once PV(j-1) consumed P(j-1): the issuer then already waited
+      // for phase j-1 of this barrier, so it can never observe two of its phases at once (a
+      // parity wait cannot tell them apart).  PV(j-1) was issued ~one softmax ago: rarely a wait.
+      if (j > 0) wait_odone(j);
       tc_fence_before();
-      mbar_arrive(b_pfull);
+      mbar_arrive(b_pfull + 8 * t);
     }
-    // epilogue: the row's Z from both halves, this half's 64 normalised acc columns, the lse
-    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // both halves past their last red read
-    red[(2 + half) * 128 + rho] = Z;
-    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-    const float Zt = Z + red[(2 + (half ^ 1)) * 128 + rho];
-    if (nt > 0) {
-      mbar_wait_parity(b_odone, (nt - 1) & 1);
-      tc_fence_after();
-    }
-    const float inv = Zt > 0.f ? 1.f / Zt : 0.f;
-    const float lse = Zt > 0.f ? M * kLn2 + logf(Zt) : -CUDART_INF_F;
-    const int slot = rvalid ? (t - 1) % W : 0;
+    // epilogue: this row's normalised (acc, lse), 32 TMEM columns at a time
+    if (nt > 0) wait_odone(nt);
+    const float inv = Z > 0.f ? 1.f / Z : 0.f;
+    const float lse = Z > 0.f ? M * kLn2 + logf(Z) : -CUDART_INF_F;
+    const int slot = rvalid ? (pos - 1) % W : 0;
     float* dst = nullptr;
     if (rvalid) {
       if (a.n_chunks == 1) {
         dst = static_cast<float*>(p.ring_acc) + (((int64_t)b * Hq + head) * W + slot) * 128;
-        if (half == 0) static_cast<float*>(p.ring_lse)[((int64_t)b * Hq + head) * W + slot] = lse;
+        static_cast<float*>(p.ring_lse)[((int64_t)b * Hq + head) * W + slot] = lse;
       } else {
         dst = static_cast<float*>(a.part) + ((((int64_t)b * a.n_rows + ri) * Hq + head) * a.n_chunks + ch) * 129;
-        if (half == 0) dst[128] = lse;
+        dst[128] = lse;
       }
     }
 #pragma unroll 1
-    for (int c = 64 * half; c < 64 * half + 64; c += 32) {
+    for (int c = 0; c < 128; c += 32) {
       uint32_t v[32];
       if (nt > 0) {
-        tmem_ld32(tm + 128 + lane_base + c, v);  // warp-collective: every lane takes part
+        tmem_ld32(tm + lane_base + tcol + 128 + c, v);  // warp-collective: every lane takes part
         tmem_wait_ld();
       } else {
 #pragma unroll
@@ -342,11 +347,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    if (rvalid && ch == 0) {  // the ring's query row (pre-RoPE, bf16 like the decode write-back), 64 dims each
+    if (rvalid && ch == 0) {  // the ring's query row (pre-RoPE, bf16 like the decode write-back)
       const int64_t qb = ((int64_t)(b * a.n_rows + ri) * Hq + head) * 128;
       __nv_bfloat16* rq = static_cast<__nv_bfloat16*>(p.ring_q) + (((int64_t)b * Hq + head) * W + slot) * 128;
-      for (int e = 64 * half; e < 64 * half + 64; ++e) rq[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
-      if (p.ring_qp && half == 0) {
+      for (int e = 0; e < 128; ++e) rq[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
+      if (p.ring_qp) {
         __nv_bfloat16* rp =
             static_cast<__nv_bfloat16*>(p.ring_qp) + (((int64_t)b * Hq + head) * W + slot) * MAC_PLANAR_DIMS;
         for (int e = 0; e < MAC_PLANAR_DIMS; ++e) rp[e] = from_f64<__nv_bfloat16>(load_in(p.q_pre, qb + e, p.in_dtype));
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) tmem_dealloc(tm, 256);
+  if (warp == 8) tmem_dealloc(tm, 512);
 }
 
 bool ring_build_tc_supported(const MacDecodeParams& p) {
@@ -375,7 +380,7 @@ cudaError_t launch_ring_build_tc(const MacDecodeParams& p, const MacRingBuildPar
   CUtensorMap mK, mV;
   if (!encode_cache_map(&mK, p.k_cache) || !encode_cache_map(&mV, p.v_cache)) return cudaErrorInvalidValue;
   const int g = p.n_q_heads / p.n_kv_heads;
-  const long n_pb = (a.n_rows + 128 / g - 1) / (128 / g);
+  const long n_pb = (a.n_rows + 256 / g - 1) / (256 / g);
   const long items = (long)p.batch * p.n_kv_heads * n_pb * a.n_chunks;
   if (items > 0x7fffffffL) return cudaErrorInvalidValue;
   ring_build_tc_kernel<<<(unsigned)items, TC_THREADS, TC_SMEM, st>>>(mK, mV, p, a);

@@ -347,9 +347,11 @@ class BatchDecodeEngine:
                 if len(cache) > 256:
                     cache.clear()
                 cache[key] = P
-        # per-call fields: the step's scan choice and no output narrowing unless the caller sets it
+        # per-call fields: the step's scan choice, no output narrowing and device-resident inputs
+        # unless the caller sets them
         P.match_mode = self._step_mode
         P.out_bf16 = None
+        P.inputs_host = 0
         return P
 
     def _build_params(self, layer: int, q, k, v, in_dt: int, force_miss: bool) -> _lib.MacDecodeParams:
@@ -446,11 +448,14 @@ class BatchDecodeEngine:
             self._accumulate_stats(layer, P)
         return self.result()
 
-    def _decode_step_ptrs(self, layer: int, q_ptr: int, k_ptr: int, v_ptr: int, in_dt: int, out_bf16: int = 0):
+    def _decode_step_ptrs(self, layer: int, q_ptr: int, k_ptr: int, v_ptr: int, in_dt: int, out_bf16: int = 0,
+                          inputs_host: bool = False):
         """decode_step on raw device pointers, optionally also writing the output narrowed to
-        bf16 at `out_bf16` (a pinned host buffer's device alias: StepGraph's zero-copy output)."""
+        bf16 at `out_bf16` (a pinned host buffer's device alias: StepGraph's zero-copy output);
+        inputs_host: q/k/v are device aliases of pinned host memory (MacDecodeParams.inputs_host)."""
         P = self._params(layer, _Ptr(q_ptr), _Ptr(k_ptr), _Ptr(v_ptr), in_dt, False)
         P.out_bf16 = out_bf16 or None
+        P.inputs_host = 1 if inputs_host else 0
         self.last_params = P
         _lib.call("mac_decode_step", P, self._stream())
         if self.track_stats and not getattr(self, "_in_prefill", False):
@@ -615,7 +620,7 @@ class BatchDecodeEngine:
         q_rows = q_rows.contiguous()
         g = cfg.n_q_heads // cfg.n_kv_heads
         vid = {"auto": 0, "mma": 1, "tcgen05": 2}[variant]
-        rows_per_cta = 8 * (8 // g) if vid == 1 else 128 // g
+        rows_per_cta = 8 * (8 // g) if vid == 1 else 256 // g
         blocks = B * cfg.n_kv_heads * -(-n_rows // rows_per_cta)
         if n_chunks is None:
             longest = int(self.seq_lens[layer].max().item())
@@ -769,9 +774,12 @@ class StepGraph:
     kernel pushes it.  (Letting the front kernel read q/k/v from the host alias directly,
     with no pull launch, measured slower: every scan CTA then waits on a host-link read.)"""
 
-    def __init__(self, eng: "BatchDecodeEngine", layer, dtype=torch.bfloat16, out_dtype=None):
+    def __init__(self, eng: "BatchDecodeEngine", layer, dtype=torch.bfloat16, out_dtype=None,
+                 host_inputs: bool = True):
         """dtype: the q/k/v input dtype; out_dtype: the host output dtype (default the engine's
-        summary dtype, f32 for bf16 storage; bf16 halves the device-to-host bytes)."""
+        summary dtype, f32 for bf16 storage; bf16 halves the device-to-host bytes);
+        host_inputs: on the bf16 two-pass path let the step read q/k/v from the pinned buffer
+        (inputs_host) instead of pulling them first."""
         cfg, B = eng.cfg, eng.batch
         self.multi = not isinstance(layer, int)
         self.layers = [int(x) for x in layer] if self.multi else [int(layer)]
@@ -780,6 +788,7 @@ class StepGraph:
         for lay in self.layers:
             eng._layer(lay)
         self.eng, self.layer = eng, (self.layers if self.multi else self.layers[0])
+        self.host_inputs = host_inputs
         n_l = len(self.layers)
         dev = eng.device
         # q, k and v of every layer share one pinned staging buffer and one device buffer:
@@ -862,6 +871,18 @@ class StepGraph:
         dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16, torch.float64: _lib.DT_F64}
         per_out = eng.o_out.numel()
         osz = self.out_host.element_size()
+        if self.direct and self.host_inputs and eng._step_mode in (0, 2):
+            # the two-pass step reads its inputs from the pinned buffer itself (inputs_host): the
+            # scan its 16 query dims, the append warps the rest, staged for the later kernels; the
+            # complete kernel writes the bf16 output into the pinned output buffer — no I/O launch
+            for i, lay in enumerate(self.layers):
+                q, k, v = self._qkv_dev[i]
+                base = self.in_dev.data_ptr()
+                al = self._in_alias.value
+                eng._decode_step_ptrs(lay, al + q.data_ptr() - base, al + k.data_ptr() - base,
+                                      al + v.data_ptr() - base, dt[q.dtype], self._out_alias.value + i * per_out * osz,
+                                      inputs_host=True)
+            return
         if self.direct:
             # inputs pulled by one zero-copy kernel; the complete kernel writes the bf16 output
             # straight into the pinned output buffer (no output launch)

@@ -299,3 +299,36 @@ def test_adaptive_dense_mode_on_a_mixed_stream():
     assert modes[0][0] == 0 and any(mm == 2 for mm, _ in modes), modes
     assert any(p & _lib.PATH_DENSE_KERNEL for mm, p in modes if mm == 2)
     assert worst <= TOL, worst
+
+
+def test_step_graph_host_inputs_equal_pulled_inputs():
+    """StepGraph's serving path with the step reading q/k/v from the pinned buffer itself
+    (MacDecodeParams.inputs_host: no input-copy launch) is bit-identical to pulling them into
+    device memory first, on the two-pass geometry, decisions and ring included."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, StepGraph, SyntheticSpec, gen_synthetic, _lib
+
+    B, hq, hkv, L, W, r = 37, 16, 4, 24, 512, 16
+    trs = [gen_synthetic(SyntheticSpec(seq_len=L, d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, seed=1300 + s))
+           for s in range(B)]
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    engs = [BatchDecodeEngine(cfg, B, L + 8, min_chunk=32) for _ in range(2)]
+    for e in engs:
+        e.match_mode = "two_pass"
+    sgs = [StepGraph(engs[0], 0, out_dtype=torch.bfloat16, host_inputs=True),
+           StepGraph(engs[1], 0, out_dtype=torch.bfloat16, host_inputs=False)]
+    q = np.stack([bf16_round(t.q_pre[:, 0]) for t in trs], 1)
+    k = np.stack([bf16_round(t.k_pre[:, 0]) for t in trs], 1)
+    v = np.stack([bf16_round(t.v[:, 0]) for t in trs], 1)
+    for m in range(1, L + 1):
+        for sg in sgs:
+            sg.q_host.copy_(torch.from_numpy(np.ascontiguousarray(q[m - 1])))
+            sg.k_host.copy_(torch.from_numpy(np.ascontiguousarray(k[m - 1])))
+            sg.v_host.copy_(torch.from_numpy(np.ascontiguousarray(v[m - 1])))
+            sg.replay()
+        torch.cuda.synchronize()
+        assert engs[0].last_params.inputs_host == 1 and engs[1].last_params.inputs_host == 0
+        assert engs[0].match_path() & _lib.PATH_TWO_PASS
+        assert torch.equal(sgs[0].out_host, sgs[1].out_host), m
+        assert torch.equal(engs[0].o_pos, engs[1].o_pos) and torch.equal(engs[0].o_hit, engs[1].o_hit), m
+    assert torch.equal(engs[0].ring_acc[0], engs[1].ring_acc[0])
+    assert torch.equal(engs[0].ring_q[0], engs[1].ring_q[0])

@@ -24,7 +24,7 @@ __device__ __host__ inline uint32_t mnmaj_off(int kk, int n, int K) {
 }
 
 __global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* A2, const __nv_bfloat16* B, const __nv_bfloat16* P,
-                      const __nv_bfloat16* V, float* S_out, float* O_out) {
+                      const __nv_bfloat16* V, float* S_out, float* O_out, float* O2_out) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* sA = sm;              // 32 KB
@@ -51,7 +51,7 @@ __global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* A2, const __n
     *reinterpret_cast<__nv_bfloat16*>(sP + kmaj_off(r, k, 128)) = P[i];
   }
   fence_proxy_async_smem();
-  if (warp == 0) tmem_alloc(smem_u32(&tmem_base), 256);
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_base), 512);
   if (tid == 0) {
     mbar_init(smem_u32(&bar), 1);
     fence_mbar_init();
@@ -80,6 +80,29 @@ __global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* A2, const __n
   }
   mbar_wait_parity(smem_u32(&bar), 0);
   tc_fence_after();
+  {  // P row -> TMEM columns 384.. (two bf16 per column), then O2 = P[tmem] . V
+    const int row = warp * 32 + lane;
+    uint32_t pv[32];
+    for (int c = 0; c < 32; ++c) {
+      __nv_bfloat162 t2;
+      t2.x = P[row * 64 + 2 * c];
+      t2.y = P[row * 64 + 2 * c + 1];
+      pv[c] = *reinterpret_cast<uint32_t*>(&t2);
+    }
+    tmem_st32(tm + ((uint32_t)(warp * 32) << 16) + 384, pv);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idO = instr_desc_bf16(128, 128, false, true);
+    for (int ks = 0; ks < 4; ++ks)
+      mma_bf16_ta(tm + 256, tm + 384 + ks * 8, sdesc_mnmajor_sw128(smem_u32(sV) + ks * 2048, 64 * 128), idO, ks > 0);
+    mma_commit(smem_u32(&bar));
+  }
+  mbar_wait_parity(smem_u32(&bar), 1);
+  tc_fence_after();
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t v[32];
   for (int c = 0; c < 64; c += 32) {
@@ -92,9 +115,14 @@ __global__ void probe(const __nv_bfloat16* A, const __nv_bfloat16* A2, const __n
     tmem_wait_ld();
     for (int j = 0; j < 32; ++j) O_out[(warp * 32 + lane) * 128 + c + j] = __uint_as_float(v[j]);
   }
+  for (int c = 0; c < 128; c += 32) {
+    tmem_ld32(tm + 256 + lane_base + c, v);
+    tmem_wait_ld();
+    for (int j = 0; j < 32; ++j) O2_out[(warp * 32 + lane) * 128 + c + j] = __uint_as_float(v[j]);
+  }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tm, 256);
+  if (warp == 0) tmem_dealloc(tm, 512);
 }
 
 int main() {
@@ -108,9 +136,9 @@ int main() {
   };
   fill(A, fA, 1.f); fill(A2, fA2, 1.f / 256); fill(B, fB, 1.f); fill(P, fP, 1.f); fill(V, fV, 1.f);
   __nv_bfloat16 *dA, *dA2, *dB, *dP, *dV;
-  float *dS, *dO;
+  float *dS, *dO, *dO2;
   cudaMalloc(&dA, nA * 2); cudaMalloc(&dA2, nA * 2); cudaMalloc(&dB, nB * 2); cudaMalloc(&dP, nP * 2);
-  cudaMalloc(&dV, nV * 2); cudaMalloc(&dS, 128 * 64 * 4); cudaMalloc(&dO, 128 * 128 * 4);
+  cudaMalloc(&dV, nV * 2); cudaMalloc(&dS, 128 * 64 * 4); cudaMalloc(&dO, 128 * 128 * 4); cudaMalloc(&dO2, 128 * 128 * 4);
   cudaMemcpy(dA, A.data(), nA * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dA2, A2.data(), nA * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), nB * 2, cudaMemcpyHostToDevice);
@@ -118,10 +146,11 @@ int main() {
   cudaMemcpy(dV, V.data(), nV * 2, cudaMemcpyHostToDevice);
   const int smem = 114688 + 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<<<1, 128, smem>>>(dA, dA2, dB, dP, dV, dS, dO);
+  probe<<<1, 128, smem>>>(dA, dA2, dB, dP, dV, dS, dO, dO2);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("kernel error: %s\n", cudaGetErrorString(e)); return 1; }
-  std::vector<float> S(128 * 64), O(128 * 128);
+  std::vector<float> S(128 * 64), O(128 * 128), O2(128 * 128);
+  cudaMemcpy(O2.data(), dO2, O2.size() * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(S.data(), dS, S.size() * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(O.data(), dO, O.size() * 4, cudaMemcpyDeviceToHost);
   double es = 0, eo = 0, ns = 0, no = 0;
@@ -137,6 +166,7 @@ int main() {
       double r = 0;
       for (int kk = 0; kk < 64; ++kk) r += (double)fP[i * 64 + kk] * fV[kk * 128 + n];
       eo = fmax(eo, fabs(r - O[i * 128 + n]));
+      eo = fmax(eo, fabs(r - O2[i * 128 + n]));
       no = fmax(no, fabs(r));
     }
   printf("S max abs err %.3e (max |S| %.2f)  O max abs err %.3e (max |O| %.2f)\n", es, ns, eo, no);
