@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(128) amend_generic_kernel(MacDecodeParams p, c
       __syncthreads();
       int split = cpos - ts + 1;  // tokens [0, split) are piece, [split, nt) band
       split = split < 0 ? 0 : (split > nt ? nt : split);
+      // One warp per (set, head): the piece set reads and rewrites S[hl][0, split), the band set
+      // S[hl][split, nt) — disjoint elements of the same row, so no barrier is needed between the
+      // max pass and the exp pass (compute-sanitizer racecheck reports these as potential WAR
+      // hazards on the shared row; profiles/r02/SUMMARY.md).
       for (int pr = warp; pr < 2 * g; pr += nwarps) {
         const int set = pr / g, hl = pr % g;
         const int a = set == 0 ? 0 : split, e = set == 0 ? split : nt;
