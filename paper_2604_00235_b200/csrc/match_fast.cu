@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 //      planned by its CTA (or by its last-decided head with PER_HEAD).
 // rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
 template <bool PER_HEAD, int kQDims>
-__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget, int defer) {
+__global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget, int defer,
+                                                     int n_append) {
   constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
   constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
   constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
@@ -272,8 +273,24 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   TL_MARK(p, TL_VERIFY_IN);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
-  const int grp = PER_HEAD ? blockIdx.x / g : blockIdx.x;
-  const int hl = PER_HEAD ? blockIdx.x % g : warp;
+  if ((int)blockIdx.x < n_append) {
+    // The step's KV append + query rotation, one warp per (request, kv head), in CTAs of their
+    // own at the head of the verify grid: it does not depend on the scan, and in the scan grid
+    // its chain of dependent loads made that grid — and so every decision — end ~4.4 us after
+    // the last scan CTA at C2.  Here it runs beside the scan and the decisions.  The amend
+    // reads its output: its band items (before their grid-dependency wait) only once every
+    // verify CTA has triggered — these after all their warps appended and fenced — and its
+    // piece items after this whole grid.
+    const int i = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (i < p.batch * Hkv) append_warp(p, i, 0, 0);
+    __threadfence();
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    return;
+  }
+  const int blk = blockIdx.x - n_append;
+  const int grp = PER_HEAD ? blk / g : blk;
+  const int hl = PER_HEAD ? blk % g : warp;
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL_MARK(p, TL_VERIFY_WAITED);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -296,6 +313,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   float qh[8];  // the query dims of this lane's chunk (kQDims + 8 ci ..)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
+    // (with append CTAs in this grid the inputs are device-resident: q_src(p) is p.q_pre)
     qh[i] = cload ? (float)load_in(q_src(p), (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
   const int m = p.seq_lens[b] + 1;
   TL_MARK_DEP(p, TL_V_M, m);
@@ -594,10 +612,13 @@ cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
   return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt);
 }
 
-cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims) {
+cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims,
+                          bool append) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads);
-  cfg.blockDim = dim3(per_head ? 32 : 32 * (p.n_q_heads / p.n_kv_heads));
+  const int warps = per_head ? 1 : p.n_q_heads / p.n_kv_heads;
+  const int n_append = append ? (p.batch * p.n_kv_heads + warps - 1) / warps : 0;
+  cfg.gridDim = dim3(n_append + (per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads));
+  cfg.blockDim = dim3(32 * warps);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -608,13 +629,13 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   const int nt = nb > 0 ? piece_target(p) : 0;
   const int defer = dense_deferred(p) ? 1 : 0;
   if (qdims == 16)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, defer)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, defer);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, defer, n_append)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, defer, n_append);
   if (qdims == 32)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, defer)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, defer);
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, defer)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, defer);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, defer, n_append)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, defer, n_append);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, defer, n_append)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, defer, n_append);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
@@ -691,19 +712,35 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const bool per_head = !per_group && p.batch * p.n_q_heads >= 148;
   const bool two_pass = do_match && front_two_pass(p);
   const FrontVariant& u = (v.two_pass && !two_pass) ? kFrontVariants[1] : v;
-  // (the append stays in the scan grid: in the verify's prologue it ran behind the scan's DRAM
-  // queue and delayed the decisions — C3 +7 us, r02 timeline)
+  // with a verify CTA per head (fewer GQA groups than SMs: C2) a whole two-pass step runs the
+  // append in CTAs of its own at the head of the verify grid (verify_kernel), so the scan grid —
+  // which the decisions wait on — is the scan alone: C2 34.2 -> 31.9 us.  With a CTA per group
+  // (C3) the scan is long enough to hide the append and the extra verify CTAs cost 2 us, and with
+  // host-resident inputs the append's PCIe reads would sit on the decisions' path (C3 e2e +9 us)
+  // (r02 A/B, profiles/r02/ab_append.sh).
+  bool app_in_verify = two_pass && per_head && !p.inputs_host && do_append && passes == 3 && !rotate_only && !plan;
+#ifdef MAC_DEV_KNOBS
+  {
+    static int knob = -1;  // MAC_APPEND_IN_VERIFY=0: append CTAs stay in the scan grid
+    if (knob < 0) {
+      const char* env = getenv("MAC_APPEND_IN_VERIFY");
+      knob = env ? atoi(env) : 1;
+    }
+    app_in_verify = app_in_verify && knob != 0;
+  }
+#endif
+  const bool app_in_front = do_append && !app_in_verify;
   const int n_match = do_match ? p.batch * p.n_q_heads * ((p.window + u.rows - 1) / u.rows) : 0;
-  const int n_append = do_append ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
-  if (n_match + n_append == 0) return cudaSuccess;
+  const int n_append = app_in_front ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
+  if (n_match + n_append == 0 && !app_in_verify) return cudaSuccess;
   if (passes & 1) {
     auto fn = (do_match && u.fn_planar && p.ring_qp) ? u.fn_planar : u.fn;
-    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, do_append ? 1 : 0, rotate_only, plan, 0);
+    fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, app_in_front ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
   if ((passes & 2) && u.two_pass && do_match) {
-    const cudaError_t e = launch_verify(p, st, per_head, u.rows, u.qdims);
+    const cudaError_t e = launch_verify(p, st, per_head, u.rows, u.qdims, app_in_verify);
     if (e || !dense_deferred(p)) return e;
     return launch_dense(p, st, u.qdims);
   }
