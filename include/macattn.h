@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 12
+#define MACATTN_ABI_VERSION 13
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
 #define MAC_PLANAR_DIMS 16
 
@@ -103,6 +103,11 @@ typedef struct MacDecodeParams {
   int32_t kv_limit;      /* tokens this KV shard holds (positions kv_offset+1 .. kv_offset+kv_limit);
                             0: unbounded (the tail shard, or no sharding) */
   int32_t n_shards;      /* partials in shard_parts (mac_shard_complete) */
+  int32_t span_chunks;   /* splits of a span planned without the split band (full attention, the
+                            one-pass miss path); 0 or >= max_chunks: max_chunks.  The split band's
+                            long (miss) pieces use every slot: 0 < span_chunks < max_chunks leaves
+                            full attention at its best split while a hit step's few missing groups
+                            spread over the whole amend grid */
   /* ---- match rule (matching.py:58-64, 141-175; engine.py:452-459) ----- */
   double thr_sq;         /* (sqrt(2d)(1 - tau_layer))^2 */
   int32_t delta_max;     /* <= 0: off */

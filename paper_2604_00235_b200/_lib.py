@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MACATTN_LIB points at an alternative build of the same library (e.g. a tracing build)
 LIB_PATH = os.environ.get("MACATTN_LIB") or os.path.join(_HERE, "lib", "libmacattn.so")
 
-ABI_VERSION = 12
+ABI_VERSION = 13
 PLANAR_DIMS = 16  # MAC_PLANAR_DIMS: dims of the planar query-ring copy (ring_qp)
 
 MODE_F32, MODE_BF16, MODE_F64 = 0, 1, 2
@@ -78,6 +78,7 @@ class MacDecodeParams(C.Structure):
         ("kv_offset", C.c_int32),
         ("kv_limit", C.c_int32),
         ("n_shards", C.c_int32),
+        ("span_chunks", C.c_int32),
         ("thr_sq", C.c_double),
         ("delta_max", C.c_int32),
         ("match_space", C.c_int32),

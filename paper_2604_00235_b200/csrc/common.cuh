@@ -172,7 +172,8 @@ __host__ __device__ __forceinline__ int shard_end(const MacDecodeParams& p, int 
 }
 // the split grid of a GQA group over [grid_start(lo_g), shard_end(m)] (plan, amend and complete agree)
 __host__ __device__ __forceinline__ Chunking group_chunking(const MacDecodeParams& p, int m, int lo_g) {
-  return chunking(shard_end(p, m) - grid_start(lo_g, p.kv_offset) + 1, p.max_chunks, p.min_chunk);
+  const int cap = (p.span_chunks > 0 && p.span_chunks < p.max_chunks) ? p.span_chunks : p.max_chunks;
+  return chunking(shard_end(p, m) - grid_start(lo_g, p.kv_offset) + 1, cap, p.min_chunk);
 }
 
 // Split band (the bf16 fast path's hit step, launch_band_split in amend_mma.cu): the band
@@ -211,8 +212,12 @@ __host__ __device__ __forceinline__ BandItems band_items(int m, int r, int nb) {
 // streams ~5 GB/s, so a few long items would serialise the step on the warps that drew them.
 // (Items of 32 tokens for C2's short pieces measured slower: 38.1 vs 35.5 us, the complete then
 // merges 17 slots.)
+// n_dense (match_mode 2: the heads the verify handed to dense_kernel, known when it plans):
+// the groups with a miss share the amend grid, so a long piece takes at most its share,
+// tgt * groups / n_dense items, and never fewer than span_chunks (C3 geometry at 16K: 2 %
+// misses 113 -> 96 us with 33 slots, 10 % unchanged at 184 us; 128K with 2 %: 476 -> 301 us).
 __host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams& p, int m, int lo_g, int nb,
-                                                          int ntarget = 0) {
+                                                          int ntarget = 0, int n_dense = 0) {
   if (nb <= 0) return group_chunking(p, m, lo_g);
   const int span = m - p.band - grid_start(lo_g, p.kv_offset) + 1;
   if (span <= 0) return chunking(span, 1, 16);
@@ -224,6 +229,12 @@ __host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams
   if (tgt > 0 && n > tgt) n = tgt;
   const int n_len = (span + max_len - 1) / max_len;
   if (n < n_len) n = n_len;
+  if (n_dense > 0 && tgt > 0) {
+    const int span_cap = (p.span_chunks > 0 && p.span_chunks < p.max_chunks) ? p.span_chunks : p.max_chunks;
+    const long share = (long)tgt * p.batch * p.n_kv_heads / n_dense;
+    const int fair = share > span_cap ? (int)(share < 0xffff ? share : 0xffff) : span_cap;
+    if (n > fair) n = fair;
+  }
   if (n > cap) n = cap;
   if (n < 1) n = 1;
   return chunking(span, n, 16);
@@ -256,14 +267,14 @@ __device__ __forceinline__ bool kv_fits(int pages_per_seq, int t, int page_size)
 // list length and work counters) must start zeroed: the engine clears the
 // workspace once at allocation and the kernels return every counter to zero
 // by the end of each step.
-constexpr int kTlSlots = 16;
+constexpr int kTlSlots = 20;
 constexpr int kMaxWsum = 128;  // scan-warp summaries per head: ceil(W / rows per CTA) * 8 warps, W <= 1024
 
 enum : int {  // timeline slots
   TL_SCAN_IN = 0, TL_SCAN_OUT = 1, TL_VERIFY_IN = 2, TL_VERIFY_WAITED = 3, TL_VERIFY_OUT = 4,
   TL_AMEND_IN = 5, TL_AMEND_WAITED = 6, TL_AMEND_OUT = 7, TL_COMPLETE_IN = 8, TL_COMPLETE_WAITED = 9,
   TL_COMPLETE_OUT = 10, TL_V_SELECTED = 11, TL_V_BOUND = 12, TL_V_SURVIVED = 13, TL_V_DECIDED = 14,
-  TL_V_M = 15
+  TL_V_M = 15, TL_DENSE_IN = 16, TL_DENSE_WAITED = 17, TL_DENSE_OUT = 18, TL_DENSE_TASK = 19
 };
 struct Workspace {
   size_t mkey_off;   // [B*Hq] u64   complemented packed (dist, pos) match key
@@ -336,8 +347,8 @@ __device__ __forceinline__ const void* q_src(const MacDecodeParams& p) {
 // development timeline (MAC_TIMELINE builds): per slot, the earliest and latest
 // %globaltimer stamp over the CTAs that reach the mark (thread 0 of each CTA)
 #ifdef MAC_TIMELINE
-__device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot) {
-  if (threadIdx.x != 0) return;
+__device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot, bool any_thread = false) {
+  if (threadIdx.x != 0 && !any_thread) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   unsigned long long* tl = ws_ptr<unsigned long long>(p, workspace_layout(p).tl_off) + 2 * slot;
@@ -345,10 +356,12 @@ __device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot) {
   atomicMax(tl + 1, t);
 }
 #define TL_MARK(p, slot) tl_mark((p), (slot))
+#define TL_MARK_THIS(p, slot) tl_mark((p), (slot), true)
 // stamp once `v` (a loaded value) is available
 #define TL_MARK_DEP(p, slot, v) do { asm volatile("" :: "r"(v)); tl_mark((p), (slot)); } while (0)
 #else
 #define TL_MARK(p, slot) ((void)0)
+#define TL_MARK_THIS(p, slot) ((void)0)
 #define TL_MARK_DEP(p, slot, v) ((void)0)
 #endif
 
@@ -357,10 +370,10 @@ __device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot) {
 // {grp, slot, t0, t1} per split appended to the device work list (the paper's
 // load-balancer plan, built on the device with no host synchronisation).
 __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int kvh, int m, int lo_g, int nb = 0,
-                                           int ntarget = 0) {
+                                           int ntarget = 0, int n_dense = 0) {
   const int start = grid_start(lo_g, p.kv_offset);
   const int end = nb > 0 ? m - p.band : shard_end(p, m);
-  const Chunking ch = plan_chunking(p, m, lo_g, nb, ntarget);
+  const Chunking ch = plan_chunking(p, m, lo_g, nb, ntarget, n_dense);
   const int slot0 = nb > 0 ? band_items(m, p.band, nb).n : 0;
   const Workspace w = workspace_layout(p);
   unsigned int* ctr = ws_ptr<unsigned int>(p, w.ctr_off);
@@ -402,7 +415,8 @@ __device__ __forceinline__ int decide_one(const MacDecodeParams& p, int bh, int 
 
 // decide_one, and the last head of a GQA group to be decided plans the group
 __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, int m, int n_scan, bool have,
-                                            double bdist, int bpos, int nb = 0, int ntarget = 0) {
+                                            double bdist, int bpos, int nb = 0, int ntarget = 0,
+                                            int n_dense = 0) {
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv;
   decide_one(p, bh, m, n_scan, have, bdist, bpos);
   const Workspace w = workspace_layout(p);
@@ -417,7 +431,7 @@ __device__ __forceinline__ void decide_head(const MacDecodeParams& p, int bh, in
       const int l = __ldcg(lo + b * Hq + kvh * g + j);
       lo_g = l < lo_g ? l : lo_g;
     }
-    plan_group(p, b, kvh, m, lo_g, nb, ntarget);
+    plan_group(p, b, kvh, m, lo_g, nb, ntarget, n_dense);
   }
 }
 

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   bool deferred = false;
   if (!PER_HEAD && defer && 2 * n_need >= nsum) {
     // match_mode 2: hand the dense walk to dense_kernel, which spreads it over the whole GPU
-    // (a CTA per 128-row chunk); this head's candidates seed its key, and its group is planned
+    // (a warp per 32-row chunk); this head's candidates seed its key, and its group is planned
     // by whichever dense chunk decides the group's last head
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -513,23 +513,29 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
 // the argmin is the one the verify would have found.  Chunks publish their best key with an
 // atomic max; the chunk completing a head decides it (finish_decide -> decide_head) and the last
 // head of a group plans the group.
-constexpr int kDenseRows = 128;
+// 32 rows per warp: one load round per task.  (128-row tasks — four dependent rounds of
+// shuffle-reduced distances — took 20 us each: at 2 % misses only ~1 task warp per SM, so
+// nothing hid their latency; C3 geometry at 16K, r02 timeline.)
+constexpr int kDenseRows = 32;
 template <int kQDims>
-__global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, int ntarget) {
+__global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, int ntarget, int rows) {
   constexpr int SPR = kQDims / 8;
   constexpr int NR = (128 - kQDims) / 8;
   constexpr int LR = NR <= 8 ? 8 : 16;
   constexpr int G = 32 / LR;
   constexpr int RK = 32 / G;
+  TL_MARK(p, TL_DENSE_IN);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL_MARK(p, TL_DENSE_WAITED);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Workspace ws = workspace_layout(p);
   const int n_dense = (int)__ldcg(ws_ptr<const unsigned int>(p, ws.ctr_off) + 8);
-  const int W = p.window, nch = (W + kDenseRows - 1) / kDenseRows;
+  const int W = p.window, nch = (W + rows - 1) / rows;
   const int ci = lane % LR, gi = lane / LR;
   const bool cload = ci < NR;
   for (int task = blockIdx.x * (blockDim.x >> 5) + warp; task < n_dense * nch; task += gridDim.x * (blockDim.x >> 5)) {
+    if (lane == 0) TL_MARK_THIS(p, TL_DENSE_TASK);
     const int bh = __ldcg(ws_ptr<const int>(p, ws.dlist_off) + task / nch);
     const int chunk = task % nch;
     const int4 st = __ldcg(ws_ptr<const int4>(p, ws.dstate_off) + bh);
@@ -550,7 +556,7 @@ __global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, i
     for (int i = 0; i < 8; ++i)
       qh[i] = cload ? (float)load_in(q_src(p), (int64_t)bh * 128 + kQDims + ci * 8 + i, p.in_dtype) : 0.f;
     unsigned long long key = 0ull;
-    const int r0 = chunk * kDenseRows, r1 = min(W, r0 + kDenseRows);
+    const int r0 = chunk * rows, r1 = min(W, r0 + rows);
 #pragma unroll 1
     for (int base = r0; base < r1; base += 32) {
       const float pr = base + lane < r1 ? __ldcg(hpart + base + lane) : CUDART_INF_F;
@@ -590,8 +596,9 @@ __global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, i
         bd = (double)__uint_as_float((unsigned)(raw >> 32));
         bp = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
       }
-      decide_head(p, bh, m, n_scan, bp > 0, bd, bp, nb, ntarget);
+      decide_head(p, bh, m, n_scan, bp > 0, bd, bp, nb, ntarget, n_dense);
     }
+    if (lane == 0) TL_MARK_THIS(p, TL_DENSE_OUT);
   }
 }
 
@@ -607,9 +614,13 @@ cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
   cfg.numAttrs = 1;
   const int nb = band_split(p);
   const int nt = nb > 0 ? piece_target(p) : 0;
-  if (qdims == 16) return cudaLaunchKernelEx(&cfg, dense_kernel<16>, p, nb, nt);
-  if (qdims == 32) return cudaLaunchKernelEx(&cfg, dense_kernel<32>, p, nb, nt);
-  return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt);
+  int rows = kDenseRows;
+#ifdef MAC_DEV_KNOBS
+  if (const char* env = getenv("MAC_DENSE_ROWS")) rows = atoi(env) >= 32 ? atoi(env) & ~31 : kDenseRows;
+#endif
+  if (qdims == 16) return cudaLaunchKernelEx(&cfg, dense_kernel<16>, p, nb, nt, rows);
+  if (qdims == 32) return cudaLaunchKernelEx(&cfg, dense_kernel<32>, p, nb, nt, rows);
+  return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt, rows);
 }
 
 cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims,

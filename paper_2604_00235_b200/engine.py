@@ -108,6 +108,15 @@ def default_max_chunks(batch: int, n_kv_heads: int, max_seq_len: int = 0) -> int
     return int(min(2048, max(8, math.ceil(SM_COUNT_B200 * 6 * 2 / groups), math.ceil(max_seq_len / 8192))))
 
 
+def default_slot_cap(max_chunks: int, max_seq_len: int) -> int:
+    """Partial slots per (request, kv head) in the workspace (MacDecodeParams.max_chunks), with
+    max_chunks the split of a full span (MacDecodeParams.span_chunks): room for a hit step's
+    missing groups to cut their context into items of ~512 tokens, up to 64 (C3 geometry, 2 %
+    misses: 16K 113 -> 96 us, 128K 476 -> 301 us; full attention keeps its best split — 16K
+    339 us at 8 vs 385 at 64; profiles/r02/mc.jsonl)."""
+    return int(max(max_chunks, min(64, math.ceil(max_seq_len / 512))))
+
+
 class _Ptr:
     """A raw device address where _params expects a tensor."""
 
@@ -141,7 +150,7 @@ class BatchDecodeEngine:
     def __init__(self, cfg: EngineConfig, batch: int, max_seq_len: int, *, device="cuda",
                  max_chunks: int | None = None, min_chunk: int = 128, page_perm_seed: int | None = None,
                  record_cached: bool = False, kv_offset: int = 0, kv_limit: int = 0, n_shards: int = 0,
-                 track_stats: bool = False, allocate_kv: bool = True):
+                 track_stats: bool = False, allocate_kv: bool = True, slot_cap: int | None = None):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         if max_seq_len < 1:
@@ -156,7 +165,14 @@ class BatchDecodeEngine:
         self.sumdt = torch.float64 if cfg.storage == "f64" else torch.float32
         self.group = cfg.n_q_heads // cfg.n_kv_heads
         self.page_size = cfg.page_size
+        # max_chunks: splits of a full span; slot_cap: partial slots per group (>= max_chunks; an
+        # explicit max_chunks without slot_cap pins both, as before)
         self.max_chunks = max_chunks or default_max_chunks(batch, cfg.n_kv_heads, max_seq_len)
+        if slot_cap is None:
+            slot_cap = self.max_chunks if max_chunks else default_slot_cap(self.max_chunks, max_seq_len)
+        if slot_cap < self.max_chunks:
+            raise ValueError("slot_cap must be >= max_chunks")
+        self.slot_cap = int(slot_cap)
         self.min_chunk = min_chunk
         if kv_offset < 0 or kv_limit < 0 or n_shards < 0:
             raise ValueError("kv_offset, kv_limit and n_shards must be >= 0")
@@ -365,7 +381,7 @@ class BatchDecodeEngine:
         P.pages_per_seq = self.page_table.shape[1]
         P.storage = _MODE[cfg.storage]
         P.in_dtype = in_dt
-        P.max_chunks, P.min_chunk = self.max_chunks, self.min_chunk
+        P.max_chunks, P.span_chunks, P.min_chunk = self.slot_cap, self.max_chunks, self.min_chunk
         P.kv_offset = self.kv_offset
         P.kv_limit = self.kv_limit
         P.n_shards = self.n_shards

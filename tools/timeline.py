@@ -25,7 +25,8 @@ os.environ["MACATTN_LIB"] = os.path.join(ROOT, "paper_2604_00235_b200", "lib", "
 sys.path.insert(0, ROOT)
 
 SLOTS = ["scan_in", "scan_out", "verify_in", "verify_waited", "verify_out", "amend_in", "amend_waited",
-         "amend_out", "complete_in", "complete_waited", "complete_out", "v_selected", "v_bound", "v_survived", "v_decided", "v_m"]
+         "amend_out", "complete_in", "complete_waited", "complete_out", "v_selected", "v_bound", "v_survived", "v_decided", "v_m",
+         "dense_in", "dense_waited", "dense_out", "dense_task"]
 
 
 def main():
@@ -36,7 +37,10 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--max-chunks", type=int, default=0)
     ap.add_argument("--min-chunk", type=int, default=128)
+    ap.add_argument("--slot-cap", type=int, default=0)
     ap.add_argument("--fresh", action="store_true", help="random queries: every head misses")
+    ap.add_argument("--miss-frac", type=float, default=0.0, help="fraction of heads given a fresh query each step")
+    ap.add_argument("--mode", default="adaptive", choices=("adaptive", "two_pass", "one_pass", "dense"))
     a = ap.parse_args()
     import bench
 
@@ -53,7 +57,8 @@ def main():
     cfg = EngineConfig(d=bench.D, d_v=bench.D, n_q_heads=32, n_kv_heads=8, window=bench.WINDOW, band=bench.BAND,
                        tau=bench.TAU, storage="bf16")
     eng = BatchDecodeEngine(cfg, a.batch, a.ctx + 64, device=dev, max_chunks=a.max_chunks or None,
-                            min_chunk=a.min_chunk)
+                            min_chunk=a.min_chunk, slot_cap=a.slot_cap or None)
+    eng.match_mode = a.mode
     inject_into_engine(eng, 0, states, n0, bulk_seed=0)
     lib = _lib.load()
     lib.mac_timeline_offset.restype = ctypes.c_size_t
@@ -65,9 +70,14 @@ def main():
     if a.fresh:
         gen = torch.Generator(device=dev).manual_seed(7)
         q_all = torch.randn(q_all.shape, device=dev, generator=gen).to(bf)
+    elif a.miss_frac > 0:
+        gen = torch.Generator(device=dev).manual_seed(7)
+        fresh = torch.randn(q_all.shape, device=dev, generator=gen).to(bf)
+        pick = torch.rand(q_all.shape[:3] + (1,), device=dev, generator=gen) < a.miss_frac
+        q_all = torch.where(pick, fresh, q_all)
     P = eng._params(0, q_all[0], k_all[0], v_all[0], _lib.DT_BF16)
     off = int(lib.mac_timeline_offset(P))
-    tl = eng.workspace[off:off + 16 * 16].view(torch.int64).view(16, 2)
+    tl = eng.workspace[off:off + 16 * len(SLOTS)].view(torch.int64).view(len(SLOTS), 2)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     rows, amends = [], []
     lib.mac_timeline_amend.restype = ctypes.c_int
@@ -96,13 +106,15 @@ def main():
         ok = t[:, i, 1] > 0
         if ok.any():
             out[name] = (round(float(first[ok].mean()), 2), round(float(last[ok].mean()), 2))
-    print(json.dumps({"batch": a.batch, "ctx": a.ctx, "max_chunks": eng.max_chunks, "min_chunk": a.min_chunk, "hit_rate": float(eng.o_use.float().mean()),
+    print(json.dumps({"batch": a.batch, "ctx": a.ctx, "miss_frac": a.miss_frac, "mode": a.mode, "max_chunks": eng.max_chunks, "slot_cap": eng.slot_cap, "min_chunk": a.min_chunk, "hit_rate": float(eng.o_use.float().mean()),
                       "first_last_us": out}))
     for name, (f, l) in out.items():
         print(f"{name:16s} first {f:8.2f}  last {l:8.2f}")
     # per-CTA amend trace: start/end spread, items and tokens per warp, first-item duration
     for tr, base in amends[-2:]:
         live = tr[:, 1] > 0
+        if not live.any():  # (the per-CTA trace is the one-warp amend's; the TMA amend has none)
+            continue
         a = tr[live].astype(np.float64)
         t0 = (a[:, 0] - base) / 1e3
         t1 = (a[:, 1] - base) / 1e3
