@@ -518,7 +518,8 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
 // nothing hid their latency; C3 geometry at 16K, r02 timeline.)
 constexpr int kDenseRows = 32;
 template <int kQDims>
-__global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, int ntarget, int rows) {
+__global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, int ntarget) {
+  constexpr int rows = kDenseRows;
   constexpr int SPR = kQDims / 8;
   constexpr int NR = (128 - kQDims) / 8;
   constexpr int LR = NR <= 8 ? 8 : 16;
@@ -604,7 +605,13 @@ __global__ void __launch_bounds__(256) dense_kernel(MacDecodeParams p, int nb, i
 
 cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(148 * 4);
+  // 4 CTAs per SM (C3 geometry at 16K: 10 % misses 197 us vs 200 at 2 and 208 at 1; 2 % the
+  // same 96 us at all three; profiles/r02/miss_regime/dense_grid_ab.jsonl)
+  int per_sm = 4;
+#ifdef MAC_DEV_KNOBS
+  if (const char* env = getenv("MAC_DENSE_CTAS")) per_sm = atoi(env) > 0 ? atoi(env) : 1;
+#endif
+  cfg.gridDim = dim3(148 * per_sm);
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -614,13 +621,9 @@ cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
   cfg.numAttrs = 1;
   const int nb = band_split(p);
   const int nt = nb > 0 ? piece_target(p) : 0;
-  int rows = kDenseRows;
-#ifdef MAC_DEV_KNOBS
-  if (const char* env = getenv("MAC_DENSE_ROWS")) rows = atoi(env) >= 32 ? atoi(env) & ~31 : kDenseRows;
-#endif
-  if (qdims == 16) return cudaLaunchKernelEx(&cfg, dense_kernel<16>, p, nb, nt, rows);
-  if (qdims == 32) return cudaLaunchKernelEx(&cfg, dense_kernel<32>, p, nb, nt, rows);
-  return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt, rows);
+  if (qdims == 16) return cudaLaunchKernelEx(&cfg, dense_kernel<16>, p, nb, nt);
+  if (qdims == 32) return cudaLaunchKernelEx(&cfg, dense_kernel<32>, p, nb, nt);
+  return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt);
 }
 
 cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims,
