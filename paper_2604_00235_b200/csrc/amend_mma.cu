@@ -20,6 +20,11 @@ __device__ unsigned long long g_amend_trace[4096 * 8];
 bool amend_tma_supported(const MacDecodeParams& p);
 int amend_tma_grid(cudaError_t* err);
 cudaError_t launch_amend_tma(const MacDecodeParams& p, cudaStream_t st, int nb);
+#ifdef MAC_DEV_KNOBS
+bool amend_tc_supported(const MacDecodeParams& p);
+int amend_tc_grid(const MacDecodeParams& p, cudaError_t* err);
+cudaError_t launch_amend_tc(const MacDecodeParams& p, cudaStream_t st, int nb);
+#endif
 
 bool amend_mma_supported(const MacDecodeParams& p) {
   const int g = p.n_q_heads / p.n_kv_heads;
@@ -183,6 +188,30 @@ static bool hit_amend_tma(const MacDecodeParams& p) {
 
 bool amend_uses_tma(const MacDecodeParams& p) { return hit_amend_tma(p); }
 
+// Whether a CTA-cooperative amend (hit_amend_tma) runs on the tcgen05 kernel (amend_tc.cu,
+// development builds only, MAC_AMEND_TC=1) rather than the mma.sync one (amend_tma.cu).
+static bool coop_amend_tc(const MacDecodeParams& p) {
+#ifdef MAC_DEV_KNOBS
+  static int forced = -2;
+  if (forced == -2) {
+    const char* env = getenv("MAC_AMEND_TC");
+    forced = env ? atoi(env) : -1;
+  }
+  return forced >= 1 && amend_tc_supported(p);
+#else
+  (void)p;
+  return false;
+#endif
+}
+// CTAs of the cooperative amend's persistent grid
+static int coop_amend_grid(const MacDecodeParams& p) {
+#ifdef MAC_DEV_KNOBS
+  if (coop_amend_tc(p)) return amend_tc_grid(p, nullptr);
+#endif
+  (void)p;
+  return amend_tma_grid(nullptr);
+}
+
 // Band items per GQA group for the split band (common.cuh band_items), 0 when the step does
 // not split it: the hit step of the fast path only — the two-pass front (whose verify kernel
 // the band overlaps, and which guarantees the append finished before this grid launches),
@@ -204,7 +233,7 @@ int band_split(const MacDecodeParams& p) {
     return 0;
   const int G = p.batch * p.n_kv_heads;
   int nb = forced > 0 ? forced
-                      : (hit_amend_tma(p) ? (amend_tma_grid(nullptr) + G - 1) / G
+                      : (hit_amend_tma(p) ? (coop_amend_grid(p) + G - 1) / G
                                           : amend_grid_full(amend_variant(false), nullptr) / G);
   if (nb > 4 && forced < 0) nb = 4;
   if (nb > p.max_chunks - 1) nb = p.max_chunks - 1;
@@ -216,7 +245,7 @@ int band_split(const MacDecodeParams& p) {
 int piece_target(const MacDecodeParams& p) {
   const int G = p.batch * p.n_kv_heads;
   if (hit_amend_tma(p)) {
-    const int t = 2 * amend_tma_grid(nullptr) / G;
+    const int t = 2 * coop_amend_grid(p) / G;
     return (t < 1 ? 1 : (t > 0xffff ? 0xffff : t)) | (32 << 16);
   }
   const int t = amend_grid_full(amend_variant(false), nullptr) / G;
@@ -232,7 +261,12 @@ cudaError_t launch_amend_mma_bf16(const MacDecodeParams& p, cudaStream_t st, boo
   const int gfull = amend_grid_full(vi, &err);
   if (err != cudaSuccess) return err;
   const int nb = full_spans ? 0 : band_split(p);
-  if (!full_spans && hit_amend_tma(p)) return launch_amend_tma(p, st, nb);
+  if (!full_spans && hit_amend_tma(p)) {
+#ifdef MAC_DEV_KNOBS
+    if (coop_amend_tc(p)) return launch_amend_tc(p, st, nb);
+#endif
+    return launch_amend_tma(p, st, nb);
+  }
   const long cap = (long)p.batch * p.n_kv_heads * p.max_chunks;
   const int grid = (int)(gfull < cap ? gfull : cap);
   // programmatic dependent launch: the grid is set up while the front kernel drains

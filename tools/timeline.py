@@ -110,6 +110,21 @@ def main():
                       "first_last_us": out}))
     for name, (f, l) in out.items():
         print(f"{name:16s} first {f:8.2f}  last {l:8.2f}")
+    if os.environ.get("MAC_AMEND_TC") == "1":  # the tcgen05 amend's per-CTA role counters
+        lib.mac_timeline_amend_tc.restype = ctypes.c_int
+        lib.mac_timeline_amend_tc.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        tc = np.zeros((1024, 16), np.uint64)
+        lib.mac_timeline_amend_tc(tc.ctypes.data, 1024)
+        live = tc[:, 1] > 0
+        a = tc[live].astype(np.float64)
+        dur = (a[:, 1] - a[:, 0]) / 1e3
+        cyc = 1.965e3  # cycles per us
+        q = lambda x: " ".join(f"{v:7.2f}" for v in np.percentile(x, [10, 50, 90]))
+        print(f"tc amend CTAs {int(live.sum())}  items/CTA p10/50/90 {q(a[:, 7])}  blocks {q(a[:, 12])}  duration us {q(dur)}")
+        for i, name in ((2, "softmax wait S"), (3, "softmax wait O"), (4, "softmax item start"),
+                        (5, "producer wait stage"), (6, "mma wait data"), (8, "sm logits/masks"),
+                        (9, "sm vote barrier"), (10, "sm rescale"), (11, "sm P write+fence"), (13, "sm finalize")):
+            print(f"  {name:20s} us p10/50/90: {q(a[:, i] / cyc)}")
     # per-CTA amend trace: start/end spread, items and tokens per warp, first-item duration
     for tr, base in amends[-2:]:
         live = tr[:, 1] > 0
