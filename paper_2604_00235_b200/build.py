@@ -39,7 +39,7 @@ if os.environ.get("MAC_DEV_KNOBS") == "1":
 # --use_fast_math only for the bf16 d = 128 fast-path kernels (their fp32 softmax and distance
 # math is written for it and parity-gated at 1e-4); the generic f32 / f64 kernels compile with
 # IEEE division, square root and denormals
-FAST_MATH = {"amend_mma.cu", "match_fast.cu", "amend_tma.cu", "ring_build.cu", "ring_build_tc.cu"}
+FAST_MATH = {"amend_mma.cu", "match_fast.cu", "amend_tma.cu", "amend_tc.cu", "ring_build.cu", "ring_build_tc.cu"}
 
 
 def nvcc() -> str:

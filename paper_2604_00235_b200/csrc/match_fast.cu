@@ -703,6 +703,14 @@ static int front_variant() {
 #endif
 }
 bool verify_per_group(const MacDecodeParams& p) {
+#ifdef MAC_DEV_KNOBS
+  static int forced = -2;
+  if (forced == -2) {
+    const char* env = getenv("MAC_VERIFY_PER_GROUP");
+    forced = env ? atoi(env) : -1;
+  }
+  if (forced >= 0) return forced == 1 && p.n_q_heads / p.n_kv_heads <= 8;
+#endif
   return p.batch * p.n_kv_heads >= 148 && p.n_q_heads / p.n_kv_heads <= 8;
 }
 // match_mode 2 (expected misses): the per-group verify defers dense heads to dense_kernel
