@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
   TL_MARK(p, TL_VERIFY_IN);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Hq = p.n_q_heads, Hkv = p.n_kv_heads, g = Hq / Hkv, W = p.window;
-  if ((int)blockIdx.x < n_append) {
+  // (compiled into the per-head verify only — the only layout that takes the append: in the
+  // per-group kernel its code alone raised the verify to 128 registers and a stack frame,
+  // +1.2 us to the first loads after the wait and +6 us to the last plan at C3)
+  if (PER_HEAD && (int)blockIdx.x < n_append) {
     // The step's KV append + query rotation, one warp per (request, kv head), in CTAs of their
     // own at the head of the verify grid: it does not depend on the scan, and in the scan grid
     // its chain of dependent loads made that grid — and so every decision — end ~4.4 us after
