@@ -13,6 +13,9 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 }
 
 // append + RoPE for one (request, kv head) by one warp; optionally plan the group as "all heads miss"
+// HOST: compiled with the staging of host-resident inputs (inputs_host); the kernels the device-
+// input steps launch leave it out (its conversions raised the scan kernel from 56 to 64 registers)
+template <bool HOST = true>
 __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, int rotate_only, int plan) {
   const int lane = threadIdx.x & 31;
   const int b = idx / p.n_kv_heads, kvh = idx % p.n_kv_heads;
@@ -73,7 +76,7 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
           const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
           const double x0 = xa[t], x1 = xb[t];
           reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
-          if (p.inputs_host) {  // host-resident inputs: stage the raw query for the later kernels
+          if (HOST && p.inputs_host) {  // host-resident inputs: stage the raw query for the later kernels
             store_in(qstage, qi, x0, p.in_dtype);
             store_in(qstage, qi + 1, x1, p.in_dtype);
           }
@@ -84,7 +87,7 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
         const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
         const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
         reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
-        if (p.inputs_host) {
+        if (HOST && p.inputs_host) {
           store_in(qstage, qi, x0, p.in_dtype);
           store_in(qstage, qi + 1, x1, p.in_dtype);
         }

@@ -44,7 +44,7 @@ __device__ __forceinline__ float dist8(const float* q, uint4 c) {
 
 }  // namespace
 
-template <int kRowsPerCta, int kMinBlocks>
+template <int kRowsPerCta, int kMinBlocks, bool HOST = true>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(MacDecodeParams p, int n_match,
                                                                                int do_append, int rotate_only,
                                                                                int plan, int /*unused*/) {
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_bf16_d128_kernel(M
   const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
   if ((int)blockIdx.x < n_append) {
     const int i = blockIdx.x * (kThreads / 32) + warp;
-    if (i < p.batch * p.n_kv_heads) append_warp(p, i, rotate_only, plan);
+    if (i < p.batch * p.n_kv_heads) append_warp<HOST>(p, i, rotate_only, plan);
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     return;
   }
@@ -158,7 +158,7 @@ __device__ __forceinline__ float dist8_f2(const unsigned long long* q2, uint4 c)
 // distance is the one-pass kernel's fp32 sum of squares split in two sums.
 // PLANAR (kQDims = MAC_PLANAR_DIMS = 16): the rows are read from ring_qp, 32 contiguous bytes
 // per row (a contiguous 32 KiB stream per head) instead of strided prefixes of ring_q.
-template <int kRowsPerCta, int kMinBlocks, int kQDims, bool PLANAR = false>
+template <int kRowsPerCta, int kMinBlocks, int kQDims, bool PLANAR = false, bool HOST = true>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDecodeParams p, int n_match,
                                                                           int do_append, int rotate_only, int plan,
                                                                           int /*unused*/) {
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   TL_MARK(p, TL_SCAN_IN);
   if ((int)blockIdx.x < n_append) {
     const int i = blockIdx.x * (kThreads / 32) + warp;
-    if (i < p.batch * p.n_kv_heads) append_warp(p, i, rotate_only, plan);
+    if (i < p.batch * p.n_kv_heads) append_warp<HOST>(p, i, rotate_only, plan);
     return;
   }
   const int W = p.window;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     // verify CTA has triggered — these after all their warps appended and fenced — and its
     // piece items after this whole grid.
     const int i = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (i < p.batch * Hkv) append_warp(p, i, 0, 0);
+    if (i < p.batch * Hkv) append_warp<false>(p, i, 0, 0);  // (never with inputs_host)
     __threadfence();
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -670,16 +670,19 @@ bool front_fast_supported(const MacDecodeParams& p) {
 // shapes scanned 3.5 and 0.8 us slower than (0).  Round-1 alternatives that lost on C3
 // (persistent tensor-core and CUDA-core scans, a DSMEM-cluster argmin, one fused step kernel)
 // were measured and not kept; their numbers are in profiles/r01/SUMMARY.md.
+using FrontFn = void (*)(MacDecodeParams, int, int, int, int, int);
 struct FrontVariant {
-  void (*fn)(MacDecodeParams, int, int, int, int, int);
+  FrontFn fn;
   int rows;
   bool two_pass;  // front_half_kernel + verify_kernel
   int qdims;      // dims of the first pass (two-pass)
-  void (*fn_planar)(MacDecodeParams, int, int, int, int, int);  // reads ring_qp when it is given
+  FrontFn fn_planar;  // reads ring_qp when it is given
+  FrontFn fn_dev, fn_planar_dev;  // the same without the host-input staging (inputs_host == 0)
 };
 static const FrontVariant kFrontVariants[] = {
-    {front_half_kernel<512, 4, 16>, 512, true, 16, front_half_kernel<512, 4, 16, true>},
-    {front_bf16_d128_kernel<128, 5>, 128, false, 0, nullptr},
+    {front_half_kernel<512, 4, 16>, 512, true, 16, front_half_kernel<512, 4, 16, true>,
+     front_half_kernel<512, 4, 16, false, false>, front_half_kernel<512, 4, 16, true, false>},
+    {front_bf16_d128_kernel<128, 5>, 128, false, 0, nullptr, front_bf16_d128_kernel<128, 5, false>, nullptr},
 #ifdef MAC_DEV_KNOBS
     {front_bf16_d128_kernel<64, 8>, 64, false, 0, nullptr},
     {front_bf16_d128_kernel<256, 3>, 256, false, 0, nullptr},
@@ -759,7 +762,9 @@ cudaError_t launch_front_bf16(const MacDecodeParams& p, cudaStream_t st, bool do
   const int n_append = app_in_front ? (p.batch * p.n_kv_heads + 7) / 8 : 0;
   if (n_match + n_append == 0 && !app_in_verify) return cudaSuccess;
   if (passes & 1) {
-    auto fn = (do_match && u.fn_planar && p.ring_qp) ? u.fn_planar : u.fn;
+    const bool planar = do_match && u.fn_planar && p.ring_qp;
+    FrontFn fn = planar ? u.fn_planar : u.fn;
+    if (!p.inputs_host) fn = planar ? (u.fn_planar_dev ? u.fn_planar_dev : fn) : (u.fn_dev ? u.fn_dev : fn);
     fn<<<n_match + n_append, kThreads, 0, st>>>(p, n_match, app_in_front ? 1 : 0, rotate_only, plan, 0);
     const cudaError_t e = cudaGetLastError();
     if (e) return e;
