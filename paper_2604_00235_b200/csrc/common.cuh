@@ -267,14 +267,15 @@ __device__ __forceinline__ bool kv_fits(int pages_per_seq, int t, int page_size)
 // list length and work counters) must start zeroed: the engine clears the
 // workspace once at allocation and the kernels return every counter to zero
 // by the end of each step.
-constexpr int kTlSlots = 20;
+constexpr int kTlSlots = 24;
 constexpr int kMaxWsum = 128;  // scan-warp summaries per head: ceil(W / rows per CTA) * 8 warps, W <= 1024
 
 enum : int {  // timeline slots
   TL_SCAN_IN = 0, TL_SCAN_OUT = 1, TL_VERIFY_IN = 2, TL_VERIFY_WAITED = 3, TL_VERIFY_OUT = 4,
   TL_AMEND_IN = 5, TL_AMEND_WAITED = 6, TL_AMEND_OUT = 7, TL_COMPLETE_IN = 8, TL_COMPLETE_WAITED = 9,
   TL_COMPLETE_OUT = 10, TL_V_SELECTED = 11, TL_V_BOUND = 12, TL_V_SURVIVED = 13, TL_V_DECIDED = 14,
-  TL_V_M = 15, TL_DENSE_IN = 16, TL_DENSE_WAITED = 17, TL_DENSE_OUT = 18, TL_DENSE_TASK = 19
+  TL_V_M = 15, TL_DENSE_IN = 16, TL_DENSE_WAITED = 17, TL_DENSE_OUT = 18, TL_DENSE_TASK = 19,
+  TL_PLAN_IN = 20, TL_PLAN_ALLOC = 21, TL_PLAN_OUT = 22
 };
 struct Workspace {
   size_t mkey_off;   // [B*Hq] u64   complemented packed (dist, pos) match key
@@ -359,10 +360,12 @@ __device__ __forceinline__ void tl_mark(const MacDecodeParams& p, int slot, bool
 #define TL_MARK_THIS(p, slot) tl_mark((p), (slot), true)
 // stamp once `v` (a loaded value) is available
 #define TL_MARK_DEP(p, slot, v) do { asm volatile("" :: "r"(v)); tl_mark((p), (slot)); } while (0)
+#define TL_MARK_DEP_THIS(p, slot, v) do { asm volatile("" :: "r"(v)); tl_mark((p), (slot), true); } while (0)
 #else
 #define TL_MARK(p, slot) ((void)0)
 #define TL_MARK_THIS(p, slot) ((void)0)
 #define TL_MARK_DEP(p, slot, v) ((void)0)
+#define TL_MARK_DEP_THIS(p, slot, v) ((void)0)
 #endif
 
 // Plan one GQA group: split grid over [grid_start(lo_g), m] (or, with the split band,
@@ -382,7 +385,9 @@ __device__ __forceinline__ void plan_group(const MacDecodeParams& p, int b, int 
   const int grp = b * p.n_kv_heads + kvh;
   ws_ptr<int>(p, w.pn_off)[grp] = ch.n | (nb << 16);
   if (ch.n == 0) return;
+  TL_MARK_THIS(p, TL_PLAN_IN);
   const unsigned base = atomicAdd(ctr, (unsigned)ch.n);
+  TL_MARK_DEP_THIS(p, TL_PLAN_ALLOC, base);
   const int n = (int)min((unsigned)ch.n, base < cap ? cap - base : 0u);  // full list: cannot happen
   for (int c = 0; c < n; ++c) {
     const int t0 = start + c * ch.len;

@@ -332,3 +332,42 @@ def test_step_graph_host_inputs_equal_pulled_inputs():
         assert torch.equal(engs[0].o_pos, engs[1].o_pos) and torch.equal(engs[0].o_hit, engs[1].o_hit), m
     assert torch.equal(engs[0].ring_acc[0], engs[1].ring_acc[0])
     assert torch.equal(engs[0].ring_q[0], engs[1].ring_q[0])
+
+
+def test_slot_capacity_spreads_missing_groups_without_changing_results():
+    """Split-KV slot capacity above the full-span split (MacDecodeParams.max_chunks > span_chunks,
+    the engine default): on a dense-mode mixed step over an 8K prompt the missing groups' pieces
+    are cut into more items than max_chunks allows, and decisions are identical and outputs within
+    TOL of an engine whose capacity is pinned to the split (ABI 12 behaviour)."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, _lib
+
+    B, hq, hkv, W, r, n = 37, 16, 4, 512, 16, 8192
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    wide = BatchDecodeEngine(cfg, B, n + 64)
+    pinned = BatchDecodeEngine(cfg, B, n + 64, max_chunks=wide.max_chunks)
+    assert wide.slot_cap > wide.max_chunks == pinned.slot_cap
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn(B, n, hq, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, n, hkv, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, n, hkv, 128, device="cuda", generator=g).bfloat16()
+    for e in (wide, pinned):
+        e.prefill(0, q, k, v, ring_build="gemm")
+        e.match_mode = "dense"
+    worst, misses = 0.0, 0
+    for s in range(3):
+        # ~10 % of the heads get a fresh query (no near-repeat: dense walk, full-context piece),
+        # the rest repeat a ring query of the last 64 positions (a hit)
+        slot = (n - 1 - torch.randint(0, 64, (B, hq), device="cuda", generator=g)) % W
+        rep = wide.ring_q[0][torch.arange(B, device="cuda")[:, None], torch.arange(hq, device="cuda")[None, :], slot]
+        fresh = torch.rand(B, hq, 1, device="cuda", generator=g) < 0.1
+        qs = torch.where(fresh, torch.randn(B, hq, 128, device="cuda", generator=g).bfloat16(), rep.bfloat16())
+        ks = torch.randn(B, hkv, 128, device="cuda", generator=g).bfloat16()
+        vs = torch.randn(B, hkv, 128, device="cuda", generator=g).bfloat16()
+        ra = wide.decode_step(0, qs, ks, vs)
+        rb = pinned.decode_step(0, qs, ks, vs)
+        assert wide.match_path() & _lib.PATH_DENSE_KERNEL
+        assert torch.equal(ra.match_hit, rb.match_hit) and torch.equal(ra.match_pos, rb.match_pos), s
+        misses += int((ra.use_hit == 0).sum())
+        worst = max(worst, ((ra.out - rb.out).norm(dim=-1) / rb.out.norm(dim=-1)).max().item())
+    assert misses > 0
+    assert worst <= TOL, worst

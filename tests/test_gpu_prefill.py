@@ -152,3 +152,34 @@ def test_prefill_gemm_and_steps_agree_on_the_next_decode():
         y = s.decode_step(0, q[:, m].contiguous(), k[:, m].contiguous(), v[:, m].contiguous())
         assert torch.equal(x.match_hit, y.match_hit) and torch.equal(x.match_pos, y.match_pos)
         assert ((x.out - y.out).norm(dim=-1) / y.out.norm(dim=-1)).max().item() <= 1e-4
+
+
+def test_tcgen05_ring_build_matches_mma_at_a_long_prompt():
+    """The two tensor-core ring builds on one long prompt (4K keys, 511 ring rows, g = 4: many
+    key tiles per CTA, both query tiles of every CTA busy): ring queries identical, summaries
+    within the 1e-4 budget (the tcgen05 kernel's multi-tile O-update barrier is exercised)."""
+    from paper_2604_00235_b200 import BatchDecodeEngine, EngineConfig, _lib
+
+    B, hq, hkv, n, W, r = 3, 16, 4, 4096, 512, 16
+    cfg = EngineConfig(d=128, d_v=128, n_q_heads=hq, n_kv_heads=hkv, window=W, band=r, storage="bf16")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn(B, n, hq, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, n, hkv, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, n, hkv, 128, device="cuda", generator=g).bfloat16()
+    engs = []
+    for variant in ("tcgen05", "mma"):
+        e = BatchDecodeEngine(cfg, B, n + 8)
+        P = e._build_params(0, q[:, 0].contiguous(), k.contiguous(), v.contiguous(), 1, False)
+        _lib.check(_lib.load().mac_prefill_kv(P, n, e._stream()), "mac_prefill_kv")
+        e._len[0] = n
+        e.build_ring(0, q[:, n - W + 1:], n_chunks=1, variant=variant)
+        engs.append(e)
+    torch.cuda.synchronize()
+    a, s = engs
+    assert torch.equal(a.ring_q[0], s.ring_q[0])
+    la, ls = a.ring_lse[0].double(), s.ring_lse[0].double()
+    fin = torch.isfinite(ls)
+    assert torch.equal(torch.isfinite(la), fin) and int(fin.sum()) == B * hq * (W - 1)
+    assert ((la[fin] - ls[fin]).abs() / ls[fin].abs().clamp_min(1.0)).max().item() <= 1e-5
+    rel = (a.ring_acc[0].double() - s.ring_acc[0].double()).norm(dim=-1) / s.ring_acc[0].double().norm(dim=-1).clamp_min(1e-30)
+    assert rel[fin].max().item() <= 1e-4, rel[fin].max().item()

@@ -26,7 +26,8 @@ sys.path.insert(0, ROOT)
 
 SLOTS = ["scan_in", "scan_out", "verify_in", "verify_waited", "verify_out", "amend_in", "amend_waited",
          "amend_out", "complete_in", "complete_waited", "complete_out", "v_selected", "v_bound", "v_survived", "v_decided", "v_m",
-         "dense_in", "dense_waited", "dense_out", "dense_task"]
+         "dense_in", "dense_waited", "dense_out", "dense_task",
+         "plan_in", "plan_alloc", "plan_out", "spare"]
 
 
 def main():
