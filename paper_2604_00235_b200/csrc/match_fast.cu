@@ -667,7 +667,9 @@ bool front_fast_supported(const MacDecodeParams& p) {
 // Development builds (-DMAC_DEV_KNOBS) add the measured alternatives, selected with
 // MAC_FRONT_VARIANT: 2-3 one-pass (64, 8), (256, 3); 4-7 two-pass (256, 4, 64), (256, 4, 32),
 // (512, 4, 32), (1024, 4, 16).  C3 step (us): 59.8 (0), 67.8 (4); the (256,6) and (512,3)
-// shapes scanned 3.5 and 0.8 us slower than (0).  Round-1 alternatives that lost on C3
+// shapes scanned 3.5 and 0.8 us slower than (0); (1024,4,16) scans 2 us faster but its verify
+// (twice the rows per scan-warp summary) takes 1.3 us longer: step 50.4 vs 49.0, C2 34.6 vs
+// 33.7 (r02, same box).  Round-1 alternatives that lost on C3
 // (persistent tensor-core and CUDA-core scans, a DSMEM-cluster argmin, one fused step kernel)
 // were measured and not kept; their numbers are in profiles/r01/SUMMARY.md.
 using FrontFn = void (*)(MacDecodeParams, int, int, int, int, int);
