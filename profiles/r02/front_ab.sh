@@ -2,7 +2,7 @@
 # dev library A/B on one box: two-pass scan shape (MAC_FRONT_VARIANT 0 = (512,4,16) product, 7 = (1024,4,16))
 O=gpurun_out/${1:-r02front}; mkdir -p $O
 DEV=$PWD/paper_2604_00235_b200/lib/libmacattn_dev.so
-for rep in 1 2; do for v in 0 7; do
+for rep in 1 2; do for v in ${VARS:-0 7}; do
   MACATTN_LIB=$DEV MAC_FRONT_VARIANT=$v timeout 600 python bench.py --steps 40 --warmup 5 --no-cpu --full-steps 2 > $O/b_${v}_$rep.json 2>/dev/null
   python -c "
 import json; d=json.loads(open('$O/b_${v}_$rep.json').readline()); k=d['kernels']
