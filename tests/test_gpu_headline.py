@@ -371,3 +371,17 @@ def test_slot_capacity_spreads_missing_groups_without_changing_results():
         worst = max(worst, ((ra.out - rb.out).norm(dim=-1) / rb.out.norm(dim=-1)).max().item())
     assert misses > 0
     assert worst <= TOL, worst
+    # the one-pass miss path and full attention split whole spans by span_chunks (= max_chunks),
+    # not by the slot capacity: both engines plan identical items, so outputs are bit-identical
+    for e in (wide, pinned):
+        e.match_mode = "one_pass"
+    qs = torch.randn(B, hq, 128, device="cuda", generator=g).bfloat16()
+    ks = torch.randn(B, hkv, 128, device="cuda", generator=g).bfloat16()
+    vs = torch.randn(B, hkv, 128, device="cuda", generator=g).bfloat16()
+    ra = wide.decode_step(0, qs, ks, vs)
+    rb = pinned.decode_step(0, qs, ks, vs)
+    assert not (wide.match_path() & _lib.PATH_TWO_PASS)
+    assert torch.equal(ra.out, rb.out)
+    fa = wide.full_decode(0, qs, ks, vs).clone()
+    fb = pinned.full_decode(0, qs, ks, vs)
+    assert torch.equal(fa, fb)
