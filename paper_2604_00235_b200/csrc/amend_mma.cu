@@ -158,6 +158,9 @@ static int amend_grid_full(int vi, cudaError_t* err) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, 32, v.smem);
+#ifdef MAC_DEV_KNOBS
+    if (const char* env = getenv("MAC_AMEND_PER_SM")) per_sm = atoi(env) > 0 ? atoi(env) : per_sm;
+#endif
     grid_full[vi] = sms * (per_sm < 1 ? 1 : per_sm);
   }
   return grid_full[vi];
