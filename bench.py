@@ -706,7 +706,7 @@ def measure_mix(args, dev):
     from paper_2604_00235_b200.synth import inject_into_engine
 
     ctx, B, hq, hkv, S = 16384, 32, 32, 8, 32
-    fracs = (0.02, 0.1, 0.3)
+    fracs = (0.005, 0.02, 0.1, 0.3)
     n0 = ctx - len(fracs) * S - 16
     states = make_states(list(range(20_000, 20_000 + B)), n0=n0, steps=S, hq=hq, hkv=hkv, d=D, dv=D, window=WINDOW,
                          band=BAND)

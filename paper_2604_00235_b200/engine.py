@@ -659,8 +659,8 @@ class BatchDecodeEngine:
         return int(_lib.load().mac_match_path(P))
 
     # miss fraction above which the adaptive engine takes the one-pass scan even where the dense
-    # kernel is available (C3 geometry at 16K: 30 % misses 371 us dense vs 315 us one-pass;
-    # 10 %: 188 vs 203 us; profiles/r02/miss_sweep_max_chunks.jsonl, bench c3mix)
+    # kernel is available (C3 geometry at 16K, final build: 20 % misses 285 us dense vs 289
+    # one-pass, 30 % 352 vs 340, 10 % 194 vs 215; profiles/r02/miss_sweep_final)
     DENSE_MAX_MISS = 0.2
 
     def _choose_match_mode(self):
@@ -674,13 +674,16 @@ class BatchDecodeEngine:
         elif self.match_mode == "dense":
             self._step_mode = 2
         else:
-            # Plain two-pass only while misses are rare: a head without a near-repeat makes its
-            # verify warp walk the whole ring (~60 us), and the verify ends with its last head.
-            # With misses, the per-group verify geometry hands those walks to dense_kernel (mode 2);
-            # other geometries, and miss-dominated steps, take the one-pass scan.
+            # Plain two-pass only while (almost) nothing misses: a head without a near-repeat makes
+            # its verify warp walk the whole ring and the verify ends with its last head — C3
+            # geometry at 16K (profiles/r02/miss_sweep_final): 0 % 48.9 us two-pass vs 63.5 dense;
+            # 1 % already 344 vs 82 (one-pass 131); 10 % 440 / 194 / 215.  So any recurring miss
+            # (two or more heads in the feedback window of 8 steps) leaves mode 0: the per-group
+            # verify geometry hands the walks to dense_kernel (mode 2); other geometries, and
+            # miss-dominated steps, take the one-pass scan.
             missed, heads = (int(x) for x in self._fb_host.tolist())
             f = missed / heads if heads > 0 else 0.0
-            if f * 100 <= 1.0:
+            if missed < 2:
                 self._step_mode = 0
             elif f <= self.DENSE_MAX_MISS and self._dense_capable():
                 self._step_mode = 2
