@@ -52,6 +52,24 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// packed fp32 pairs (sm_100 FADD2) and the three-input max (FMNMX3): the softmax rows run at
+// about 30 % fewer instructions for the same roundings.  (Measured: C3 ring 125.9 vs 125.4 ms,
+// C2 7.8 vs 8.0 ms — the kernel is not issue-bound; ncu: tensor pipe ~50 % active, r02.)
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -255,28 +273,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int c = 0; c < 64; ++c) l[c] = (kt + c <= hi_mask) ? l[c] : -CUDART_INF_F;
       }
       float mx;
-      {
-        float m32[32];
+      {  // three-input max tree: 64 -> 22 -> 8 -> 3 -> 1
+        float m22[22];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) m32[c] = fmaxf(l[c], l[c + 32]);
+        for (int c = 0; c < 21; ++c) m22[c] = max3f(l[3 * c], l[3 * c + 1], l[3 * c + 2]);
+        m22[21] = l[63];
+        float m8[8];
 #pragma unroll
-        for (int w = 16; w > 0; w >>= 1)
-#pragma unroll
-          for (int c = 0; c < w; ++c) m32[c] = fmaxf(m32[c], m32[c + w]);
-        mx = m32[0];
+        for (int c = 0; c < 7; ++c) m8[c] = max3f(m22[3 * c], m22[3 * c + 1], m22[3 * c + 2]);
+        m8[7] = m22[21];
+        mx = max3f(max3f(m8[0], m8[1], m8[2]), max3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       }
       const float Mn = (M == -CUDART_INF_F || mx > M + 8.f) ? fmaxf(M, mx) : M;
       const float alpha = (M == -CUDART_INF_F || Mn == M) ? 1.f : exp2f(M - Mn);
       float zs;
       {
         const float nm = (Mn == -CUDART_INF_F) ? 0.f : -Mn;  // a fully masked row: exp2(-inf) = 0
-        float z8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const unsigned long long nm2 = f2pack(nm, nm);
+        unsigned long long z4[4] = {0ull, 0ull, 0ull, 0ull};  // the pairs (c & 7) = (0,1) (2,3) (4,5) (6,7)
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          l[c] = exp2f(l[c] + nm);
-          z8[c & 7] += l[c];
+        for (int c = 0; c < 64; c += 2) {
+          const unsigned long long x = add2(f2pack(l[c], l[c + 1]), nm2);
+          l[c] = exp2f(f2lo(x));
+          l[c + 1] = exp2f(f2hi(x));
+          z4[(c & 7) >> 1] = add2(z4[(c & 7) >> 1], f2pack(l[c], l[c + 1]));
         }
-        zs = ((z8[0] + z8[1]) + (z8[2] + z8[3])) + ((z8[4] + z8[5]) + (z8[6] + z8[7]));
+        zs = ((f2lo(z4[0]) + f2hi(z4[0])) + (f2lo(z4[1]) + f2hi(z4[1]))) +
+             ((f2lo(z4[2]) + f2hi(z4[2])) + (f2lo(z4[3]) + f2hi(z4[3])));
       }
       Z = Z * alpha + zs;
       if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O row *= alpha once PV(j-1) has landed
@@ -299,7 +322,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int c = 0; c < 32; ++c) {
           const float x0 = l[2 * c], x1 = l[2 * c + 1];
           ph[c] = pack2(x0, x1);
-          pl[c] = pack2(x0 - __uint_as_float(ph[c] << 16), x1 - __uint_as_float(ph[c] & 0xffff0000u));
+          // lo = x - hi for both halves in one FADD2 (hi negated through its sign bits)
+          const unsigned long long nh = f2pack(__uint_as_float((ph[c] << 16) ^ 0x80000000u),
+                                               __uint_as_float((ph[c] & 0xffff0000u) ^ 0x80000000u));
+          const unsigned long long lo = add2(f2pack(x0, x1), nh);
+          pl[c] = pack2(f2lo(lo), f2hi(lo));
         }
         tmem_st32(sa, ph);
         tmem_st32(sa + 32, pl);
