@@ -169,13 +169,13 @@ static int amend_grid_full(int vi, cudaError_t* err) {
 // Which kernel runs the hit step's amend.  With fewer GQA groups than SMs (C2: B = 8, 8 KV heads)
 // each group's items are long and few, and the one-warp kernel streams an item at ~5 GB/s per
 // warp (its 2-stage lookahead covers one DRAM round trip per 32 tokens), so the TMA kernel
-// (amend_tma.cu: a producer warp keeps three 32-token stages in flight per CTA, three consumer
+// (amend_tma.cu: a producer warp keeps four 32-token stages in flight per CTA, two consumer
 // warps share each item) ends the C2 amend 6 us earlier; with many groups (C3: 256) the one-warp
 // kernel's 6-7 independent warps per SM win (in-step timelines, profiles/r02/SUMMARY.md).  Steps
 // the engine expects to miss (match_mode 1 / 2) also take the TMA kernel: a missing head's group
 // reads its whole context in a few long items, which the one-warp kernel streams slowly (C3
 // geometry at 16K with 2% misses: 118 vs 170 us per step).  Development builds can force either
-// with MAC_AMEND_TMA=0 / 1 (3 consumers, 3 stages) / 2 (6 consumers, 6 stages).
+// with MAC_AMEND_TMA=0 / 1, and pick the TMA kernel's other geometries with 2-4 (amend_tma.cu).
 static bool hit_amend_tma(const MacDecodeParams& p) {
   bool want = p.batch * p.n_kv_heads < 148 || p.match_mode != 0;
 #ifdef MAC_DEV_KNOBS

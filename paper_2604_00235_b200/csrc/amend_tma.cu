@@ -394,15 +394,19 @@ bool encode_cache_map(CUtensorMap* m, const void* ptr) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// variants (MAC_AMEND_TMA = 1, 2): (consumers, stages, CTAs per SM)
+// variants (consumers, stages, CTAs per SM); development builds select 2-4 with MAC_AMEND_TMA
 struct TmaVariant {
   void (*fn)(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, MacDecodeParams, int);
   int threads, smem;
 };
 static const TmaVariant kTma[] = {
-    {amend_tma_kernel<3, 3, 2>, TmaRing<3, 3>::THREADS, TmaRing<3, 3>::SMEM},
+    // 2 consumers, 4 stages, 2 CTAs per SM (same box, dev A/B vs 3 / 3 / 2: C2 34.3 vs 34.6 us;
+    // C3 geometry at 16K in dense mode, 0.5 / 2 / 10 % misses: 71.5 / 87.5 / 180 vs 74 / 92 / 194)
+    {amend_tma_kernel<2, 4, 2>, TmaRing<2, 4>::THREADS, TmaRing<2, 4>::SMEM},
 #ifdef MAC_DEV_KNOBS
-    {amend_tma_kernel<6, 6, 1>, TmaRing<6, 6>::THREADS, TmaRing<6, 6>::SMEM},
+    {amend_tma_kernel<6, 6, 1>, TmaRing<6, 6>::THREADS, TmaRing<6, 6>::SMEM},  // MAC_AMEND_TMA=2
+    {amend_tma_kernel<2, 2, 4>, TmaRing<2, 2>::THREADS, TmaRing<2, 2>::SMEM},  // MAC_AMEND_TMA=3 (38.3 at C2)
+    {amend_tma_kernel<3, 3, 2>, TmaRing<3, 3>::THREADS, TmaRing<3, 3>::SMEM},  // MAC_AMEND_TMA=4 (round 2's first)
 #endif
 };
 static int tma_variant() {
@@ -410,7 +414,7 @@ static int tma_variant() {
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("MAC_AMEND_TMA");
-    v = (env && atoi(env) == 2) ? 1 : 0;
+    v = env ? (atoi(env) == 2 ? 1 : atoi(env) == 3 ? 2 : atoi(env) == 4 ? 3 : 0) : 0;
   }
   return v;
 #else
