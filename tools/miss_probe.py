@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--mode", default="adaptive", choices=("adaptive", "two_pass", "one_pass", "dense"))
     ap.add_argument("--max-chunks", type=int, default=0, help="splits of a full span per group (0: engine default)")
     ap.add_argument("--slot-cap", type=int, default=0, help="partial slots per group (0: engine default)")
+    ap.add_argument("--min-chunk", type=int, default=128)
     a = ap.parse_args()
     import bench
 
@@ -46,7 +47,7 @@ def main():
     cfg = EngineConfig(d=bench.D, d_v=bench.D, n_q_heads=32, n_kv_heads=8, window=bench.WINDOW, band=bench.BAND,
                        tau=bench.TAU, storage="bf16")
     eng = BatchDecodeEngine(cfg, a.batch, a.ctx + 64, device=dev, max_chunks=a.max_chunks or None,
-                           slot_cap=a.slot_cap or None)
+                           slot_cap=a.slot_cap or None, min_chunk=a.min_chunk)
     eng.match_mode = a.mode
     inject_into_engine(eng, 0, states, n0, bulk_seed=0)
     g = torch.Generator(device=dev).manual_seed(7)
@@ -72,7 +73,7 @@ def main():
                 acc.append(e0.elapsed_time(e1) * 1e3)
         miss.append(1.0 - float(eng.o_use.float().mean()))
     print(json.dumps({"ctx": a.ctx, "batch": a.batch, "mode": a.mode, "miss_frac": a.miss_frac,
-                      "max_chunks": eng.max_chunks, "slot_cap": eng.slot_cap, "amend_tma": os.environ.get("MAC_AMEND_TMA", ""),
+                      "max_chunks": eng.max_chunks, "slot_cap": eng.slot_cap, "min_chunk": a.min_chunk, "amend_tma": os.environ.get("MAC_AMEND_TMA", ""),
                       "miss_rate": float(np.mean(miss)),
                       "mac_us": float(np.mean(mac)), "full_us": float(np.mean(full)),
                       "mac_us_median": float(np.median(mac)), "full_us_median": float(np.median(full))}))
