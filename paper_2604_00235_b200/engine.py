@@ -659,8 +659,8 @@ class BatchDecodeEngine:
         return int(_lib.load().mac_match_path(P))
 
     # miss fraction above which the adaptive engine takes the one-pass scan even where the dense
-    # kernel is available (C3 geometry at 16K, final build: 20 % misses 285 us dense vs 289
-    # one-pass, 30 % 352 vs 340, 10 % 194 vs 215; profiles/r02/miss_sweep_final)
+    # kernel is available (C3 geometry at 16K, final build: 10 % misses 180 us dense vs 201
+    # one-pass, 20 % 263 vs 269, 30 % 330 vs 317, 40 % 349 vs 331; profiles/r02/SUMMARY.md)
     DENSE_MAX_MISS = 0.2
 
     def _choose_match_mode(self):
