@@ -249,7 +249,11 @@ int piece_target(const MacDecodeParams& p) {
   const int G = p.batch * p.n_kv_heads;
   if (hit_amend_tma(p)) {
     const int t = 2 * coop_amend_grid(p) / G;
-    return (t < 1 ? 1 : (t > 0xffff ? 0xffff : t)) | (32 << 16);
+    int subs = 32;  // longest item: 32 sub-tiles of 16 tokens
+#ifdef MAC_DEV_KNOBS
+    if (const char* env = getenv("MAC_TMA_MAXSUB")) subs = atoi(env) > 0 ? atoi(env) : subs;
+#endif
+    return (t < 1 ? 1 : (t > 0xffff ? 0xffff : t)) | (subs << 16);
   }
   const int t = amend_grid_full(amend_variant(false), nullptr) / G;
   return t < 1 ? 1 : t;
