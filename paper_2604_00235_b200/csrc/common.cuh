@@ -71,6 +71,33 @@ __device__ __forceinline__ void store_in(void* p, int64_t i, double v, int dt) {
   else static_cast<double*>(p)[i] = v;
 }
 
+// a pair of consecutive elements (index i even) in one load: with host-resident inputs every load
+// instruction is its own PCIe read, so the pairs halve the append's requests
+__device__ __forceinline__ void load_pair(const void* p, int64_t i, int dt, double& x0, double& x1) {
+  if (dt == MAC_DT_BF16) {
+    const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(p) + i);
+    x0 = (double)__bfloat162float(v.x);
+    x1 = (double)__bfloat162float(v.y);
+  } else if (dt == MAC_DT_F32) {
+    const float2 v = *reinterpret_cast<const float2*>(static_cast<const float*>(p) + i);
+    x0 = (double)v.x;
+    x1 = (double)v.y;
+  } else {
+    const double2 v = *reinterpret_cast<const double2*>(static_cast<const double*>(p) + i);
+    x0 = v.x;
+    x1 = v.y;
+  }
+}
+__device__ __forceinline__ void store_pair(void* p, int64_t i, double x0, double x1, int dt) {
+  if (dt == MAC_DT_F32) *reinterpret_cast<float2*>(static_cast<float*>(p) + i) = make_float2((float)x0, (float)x1);
+  else if (dt == MAC_DT_BF16) {
+    __nv_bfloat162 v;
+    v.x = __double2bfloat16(x0);
+    v.y = __double2bfloat16(x1);
+    *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p) + i) = v;
+  } else *reinterpret_cast<double2*>(static_cast<double*>(p) + i) = make_double2(x0, x1);
+}
+
 // element load from an input tensor of runtime dtype (MAC_DT_*)
 __device__ __forceinline__ double load_in(const void* p, int64_t i, int dt) {
   if (dt == MAC_DT_F32) return (double)static_cast<const float*>(p)[i];

@@ -13,8 +13,10 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 }
 
 // append + RoPE for one (request, kv head) by one warp; optionally plan the group as "all heads miss"
-// HOST: compiled with the staging of host-resident inputs (inputs_host); the kernels the device-
-// input steps launch leave it out (its conversions raised the scan kernel from 56 to 64 registers)
+// HOST: compiled with the staging of host-resident inputs (inputs_host) and with pair / 8-byte
+// loads of q, k, v (each load instruction is a PCIe read there: C3 e2e 65.6 -> 63.7 us); the
+// kernels the device-input steps launch leave both out (they raised the scan kernel from 56 to
+// 61-64 registers: +0.4 us on the device step)
 template <bool HOST = true>
 __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, int rotate_only, int plan) {
   const int lane = threadIdx.x & 31;
@@ -55,7 +57,9 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
     sincos((double)m * p.rope_freqs[j], &s, &c);
     if (store) {
       const int64_t ki = ((int64_t)b * p.n_kv_heads + kvh) * 128 + 2 * j;
-      const double x0 = load_in(p.k_pre, ki, p.in_dtype), x1 = load_in(p.k_pre, ki + 1, p.in_dtype);
+      double x0, x1;
+      if (HOST) load_pair(p.k_pre, ki, p.in_dtype, x0, x1);
+      else x0 = load_in(p.k_pre, ki, p.in_dtype), x1 = load_in(p.k_pre, ki + 1, p.in_dtype);
       __nv_bfloat162 kk;
       kk.x = from_f64<__nv_bfloat16>(x0 * c - x1 * s);
       kk.y = from_f64<__nv_bfloat16>(x0 * s + x1 * c);
@@ -67,8 +71,15 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
-          xa[t] = h0 + t < g ? (float)load_in(p.q_pre, qi, p.in_dtype) : 0.f;
-          xb[t] = h0 + t < g ? (float)load_in(p.q_pre, qi + 1, p.in_dtype) : 0.f;
+          if (HOST) {
+            double d0 = 0.0, d1 = 0.0;
+            if (h0 + t < g) load_pair(p.q_pre, qi, p.in_dtype, d0, d1);
+            xa[t] = (float)d0;
+            xb[t] = (float)d1;
+          } else {
+            xa[t] = h0 + t < g ? (float)load_in(p.q_pre, qi, p.in_dtype) : 0.f;
+            xb[t] = h0 + t < g ? (float)load_in(p.q_pre, qi + 1, p.in_dtype) : 0.f;
+          }
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -76,28 +87,40 @@ __device__ __forceinline__ void append_warp(const MacDecodeParams& p, int idx, i
           const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + h0 + t) * 128 + 2 * j;
           const double x0 = xa[t], x1 = xb[t];
           reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
-          if (HOST && p.inputs_host) {  // host-resident inputs: stage the raw query for the later kernels
-            store_in(qstage, qi, x0, p.in_dtype);
-            store_in(qstage, qi + 1, x1, p.in_dtype);
-          }
+          if (HOST && p.inputs_host)  // host-resident inputs: stage the raw query for the later kernels
+            store_pair(qstage, qi, x0, x1, p.in_dtype);
         }
       }
     } else {
       for (int hl = 0; hl < g; ++hl) {
         const int64_t qi = ((int64_t)b * p.n_q_heads + kvh * g + hl) * 128 + 2 * j;
-        const double x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
+        double x0, x1;
+        if (HOST) load_pair(p.q_pre, qi, p.in_dtype, x0, x1);
+        else x0 = load_in(p.q_pre, qi, p.in_dtype), x1 = load_in(p.q_pre, qi + 1, p.in_dtype);
         reinterpret_cast<float2*>(qrot + qi)[0] = make_float2((float)(x0 * c - x1 * s), (float)(x0 * s + x1 * c));
-        if (HOST && p.inputs_host) {
-          store_in(qstage, qi, x0, p.in_dtype);
-          store_in(qstage, qi + 1, x1, p.in_dtype);
-        }
+        if (HOST && p.inputs_host) store_pair(qstage, qi, x0, x1, p.in_dtype);
       }
     }
   }
-  if (store)
+  if (store && !HOST) {
     for (int e = lane; e < 128; e += 32)
       vc[row * 128 + e] =
           from_f64<__nv_bfloat16>(load_in(p.v_in, ((int64_t)b * p.n_kv_heads + kvh) * 128 + e, p.in_dtype));
+  } else if (store) {  // host inputs: four consecutive values a lane (two pair loads, one 8-byte store)
+    const int64_t vi = ((int64_t)b * p.n_kv_heads + kvh) * 128 + 4 * lane;
+    double v0, v1, v2, v3;
+    load_pair(p.v_in, vi, p.in_dtype, v0, v1);
+    load_pair(p.v_in, vi + 2, p.in_dtype, v2, v3);
+    __nv_bfloat162 lo, hi;
+    lo.x = from_f64<__nv_bfloat16>(v0);
+    lo.y = from_f64<__nv_bfloat16>(v1);
+    hi.x = from_f64<__nv_bfloat16>(v2);
+    hi.y = from_f64<__nv_bfloat16>(v3);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&lo);
+    w.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(vc + row * 128 + 4 * lane) = w;
+  }
   if (plan && lane == 0) {
     int* lo = ws_ptr<int>(p, w.lo_off);
     for (int hl = 0; hl < g; ++hl) lo[b * p.n_q_heads + kvh * g + hl] = 1;
