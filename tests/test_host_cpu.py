@@ -288,3 +288,24 @@ def test_new_entry_points_validate_without_gpu():
     assert lib.mac_match_rows(m, None) == 1001
     assert lib.mac_remove_summaries(1, 4, None, a, a, a, 1e-6, a, a, a, None) == 1001
     assert lib.mac_rope_rotate(1, 3, a, a, a, a, None) == 1002
+
+
+def test_split_defaults_and_span_chunks_field():
+    """The engine's split-KV defaults (engine.py default_max_chunks / default_slot_cap) and the ABI
+    13 span_chunks field: the slot capacity never falls below the full-span split, grows with the
+    context up to 64, and the ctypes mirror carries the field where the header declares it."""
+    from paper_2604_00235_b200 import _lib
+    from paper_2604_00235_b200.engine import default_max_chunks, default_slot_cap
+
+    mc = default_max_chunks(32, 8, 16384 + 64)  # C3 geometry at 16K: 8 splits of a full span
+    assert mc == 8
+    assert default_slot_cap(mc, 16384 + 64) == 33  # ~512-token items for a missing group
+    assert default_slot_cap(17, 131072) == 64  # capped
+    assert default_slot_cap(222, 524288) == 222  # never below the span split (C4)
+    for n in (64, 1024, 8192, 65536):
+        assert default_slot_cap(default_max_chunks(4, 8, n), n) >= default_max_chunks(4, 8, n)
+    names = [f[0] for f in _lib.MacDecodeParams._fields_]
+    assert names.index("span_chunks") == names.index("n_shards") + 1
+    with open(os.path.join(ROOT, "include", "macattn.h")) as fh:
+        hdr = fh.read()
+    assert re.search(r"int32_t n_shards;.*\n\s*int32_t span_chunks;", hdr)
