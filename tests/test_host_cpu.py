@@ -309,3 +309,27 @@ def test_split_defaults_and_span_chunks_field():
     with open(os.path.join(ROOT, "include", "macattn.h")) as fh:
         hdr = fh.read()
     assert re.search(r"int32_t n_shards;.*\n\s*int32_t span_chunks;", hdr)
+
+
+def test_adaptive_scan_policy():
+    """BatchDecodeEngine._choose_match_mode on the published {missed, heads} feedback: the plain
+    two-pass scan while at most one head missed in the window, dense mode up to DENSE_MAX_MISS
+    where the geometry has it (else the one-pass scan), the one-pass scan above; pinned modes win."""
+    import torch
+
+    from paper_2604_00235_b200 import BatchDecodeEngine
+
+    def mode(missed, heads, dense=True, pin="adaptive"):
+        e = object.__new__(BatchDecodeEngine)
+        e.match_mode = pin
+        e._fb_host = torch.tensor([missed, heads], dtype=torch.int32)
+        e._dense_cap = dense
+        e._choose_match_mode()
+        return e._step_mode
+
+    H = 8 * 1024
+    assert mode(0, H) == 0 and mode(1, H) == 0
+    assert mode(2, H) == 2 and mode(int(0.2 * H), H) == 2
+    assert mode(2, H, dense=False) == 1
+    assert mode(int(0.3 * H), H) == 1
+    assert mode(0, H, pin="one_pass") == 1 and mode(H, H, pin="two_pass") == 0 and mode(0, H, pin="dense") == 2
