@@ -218,8 +218,8 @@ static int coop_amend_grid(const MacDecodeParams& p) {
 // Band items per GQA group for the split band (common.cuh band_items), 0 when the step does
 // not split it: the hit step of the fast path only — the two-pass front (whose verify kernel
 // the band overlaps, and which guarantees the append finished before this grid launches),
-// one KV shard, r > 0.  As many items per group as the persistent grid has warps per group
-// (1..4).  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
+// one KV shard, r > 0.  The one-warp amend: as many items per group as its grid has warps per
+// group (1..4); the TMA-fed amend: one.  In development builds MAC_BAND_SPLIT=0 turns it off, =n forces n items.  The verify
 // kernel's plan and this launch call it with the same parameters, so they always agree.
 int band_split(const MacDecodeParams& p) {
 #ifdef MAC_DEV_KNOBS
@@ -235,9 +235,9 @@ int band_split(const MacDecodeParams& p) {
       p.band <= 0)
     return 0;
   const int G = p.batch * p.n_kv_heads;
-  int nb = forced > 0 ? forced
-                      : (hit_amend_tma(p) ? (coop_amend_grid(p) + G - 1) / G
-                                          : amend_grid_full(amend_variant(false), nullptr) / G);
+  // the TMA-fed amend: one band item per group (C2: 33.3 vs 34.2 us with 4; dense-mode steps at
+  // 16K 0.5 / 2 / 10 % misses 71.5 / 86.7 / 179.8 vs 71.8 / 87.8 / 180.1; r02 same-box sweeps)
+  int nb = forced > 0 ? forced : (hit_amend_tma(p) ? 1 : amend_grid_full(amend_variant(false), nullptr) / G);
   if (nb > 4 && forced < 0) nb = 4;
   if (nb > p.max_chunks - 1) nb = p.max_chunks - 1;
   return nb < 1 ? 0 : nb;
