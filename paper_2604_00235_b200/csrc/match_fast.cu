@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
 // rows: ring rows per scan CTA of the launched scan variant; kQDims: dims its pass covered.
 template <bool PER_HEAD, int kQDims>
 __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows, int nb, int ntarget, int defer,
-                                                     int n_append) {
+                                                     int n_append, int clustered) {
   constexpr int SPR = kQDims / 8, RPW = 32 / SPR;  // the scan's lanes per row, rows per warp-load
   constexpr int NR = (128 - kQDims) / 8;           // remaining 16-byte chunks per row
   constexpr int LR = NR <= 8 ? 8 : 16;             // lanes per row here (NR of them load)
@@ -488,7 +488,31 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
     bpos = (int)(0xffffffffu - (unsigned)(raw & 0xffffffffull));
   }
   if (PER_HEAD) {
-    if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos, nb, ntarget);  // the group's last head plans it
+    if (!clustered) {
+      if (lane == 0) decide_head(p, bh, m, n_scan, bpos > 0, bd, bpos, nb, ntarget);  // the group's last head plans it
+      TL_MARK(p, TL_VERIFY_OUT);
+      return;
+    }
+    // The group's g head CTAs are one thread-block cluster (launch_verify): each head's first
+    // token goes into the leader CTA's shared memory (DSMEM) and one cluster barrier replaces
+    // decide_head's chain through L2 (release fence, group-counter atomic, the lo loads of the
+    // last arriver); the leader (cluster rank 0 = head 0 of the group) plans the group.
+    __shared__ int s_lo[8];
+    int lo = 0;
+    if (lane == 0) lo = decide_one(p, bh, m, n_scan, bpos > 0, bd, bpos);
+    if (lane == 0) {
+      const uint32_t la = (uint32_t)__cvta_generic_to_shared(&s_lo[hl]);
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(0));
+      asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(ra), "r"(lo) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    TL_MARK(p, TL_V_DECIDED);
+    if (hl == 0 && lane == 0) {
+      int lo_g = m;
+      for (int j = 0; j < g; ++j) lo_g = s_lo[j] < lo_g ? s_lo[j] : lo_g;
+      plan_group(p, b, kvh, m, lo_g, nb, ntarget);
+    }
     TL_MARK(p, TL_VERIFY_OUT);
     return;
   }
@@ -632,27 +656,36 @@ cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
 cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_head, int rows, int qdims,
                           bool append) {
   cudaLaunchConfig_t cfg = {};
-  const int warps = per_head ? 1 : p.n_q_heads / p.n_kv_heads;
-  const int n_append = append ? (p.batch * p.n_kv_heads + warps - 1) / warps : 0;
+  const int g = p.n_q_heads / p.n_kv_heads;
+  const int warps = per_head ? 1 : g;
+  // per-head verify: a GQA group's head CTAs form one cluster (exchange through DSMEM, see
+  // verify_kernel); the append CTAs ahead of them are padded to whole clusters
+  const int clustered = per_head && g > 1 && g <= 8 ? 1 : 0;
+  int n_append = append ? (p.batch * p.n_kv_heads + warps - 1) / warps : 0;
+  if (clustered) n_append = (n_append + g - 1) / g * g;
   cfg.gridDim = dim3(n_append + (per_head ? p.batch * p.n_q_heads : p.batch * p.n_kv_heads));
   cfg.blockDim = dim3(32 * warps);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = clustered ? g : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = clustered ? 2 : 1;
   const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
   const int nt = nb > 0 ? piece_target(p) : 0;
   const int defer = dense_deferred(p) ? 1 : 0;
   if (qdims == 16)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, defer, n_append)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, defer, n_append);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, defer, n_append, clustered)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, defer, n_append, clustered);
   if (qdims == 32)
-    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, defer, n_append)
-                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, defer, n_append);
-  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, defer, n_append)
-                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, defer, n_append);
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 32>, p, rows, nb, nt, defer, n_append, clustered)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 32>, p, rows, nb, nt, defer, n_append, clustered);
+  return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 64>, p, rows, nb, nt, defer, n_append, clustered)
+                  : cudaLaunchKernelEx(&cfg, verify_kernel<false, 64>, p, rows, nb, nt, defer, n_append, clustered);
 }
 
 bool match_fast_supported(const MacDecodeParams& p) {
