@@ -306,7 +306,7 @@ def test_step_graph_across_layers():
         StepGraph(graphed, [0, 0])
 
 
-@pytest.mark.parametrize("B,hq,hkv", [(37, 16, 4), (10, 16, 2)])
+@pytest.mark.parametrize("B,hq,hkv", [(37, 16, 4), (10, 16, 2), (5, 32, 8)])
 def test_two_pass_match_large_batch_replay(B, hq, hkv):
     """Enough heads for the two-pass match (planar 16-dim scan + verify; rings of W >= 512): one
     verify CTA per GQA group (B * Hkv >= 148) or per head (fewer groups, B * Hq >= 148);
