@@ -38,6 +38,10 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, 
   const int lane = threadIdx.x;
   const uint32_t sm = smem_u32(smem);
   TL_MARK(p, TL_AMEND_IN);
+#ifdef MAC_TIMELINE
+  unsigned long long tr_in, tr_band_end = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_in));
+#endif
   if (nb > 0) {
     // Split band (common.cuh band_items): the band items need only what the front kernel
     // (the verify kernel's predecessor, complete before any of this grid launched) wrote —
@@ -54,6 +58,9 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, 
       amend_mma_item<ST, true>(p, make_int4(grp, c, t0, min(m, t0 + bi.len - 1)), sm, []() {});
     }
   }
+#ifdef MAC_TIMELINE
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_band_end));
+#endif
   // programmatic dependent launch: wait for the front kernel's plan before touching it
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL_MARK(p, TL_AMEND_WAITED);
@@ -108,6 +115,8 @@ __global__ void __launch_bounds__(32, MINB) amend_mma_kernel(MacDecodeParams p, 
     g_amend_trace[blockIdx.x * 8 + 3] = tr_tokens;
     g_amend_trace[blockIdx.x * 8 + 4] = tr_first;
     g_amend_trace[blockIdx.x * 8 + 5] = tr_first_tok;
+    g_amend_trace[blockIdx.x * 8 + 6] = tr_in;
+    g_amend_trace[blockIdx.x * 8 + 7] = (nb > 0 && (int)blockIdx.x < p.batch * p.n_kv_heads * nb) ? tr_band_end : 0;
   }
 #endif
   TL_MARK(p, TL_AMEND_OUT);

@@ -138,6 +138,12 @@ def main():
         items, toks = a[:, 2], a[:, 3]
         q = lambda x: " ".join(f"{v:7.2f}" for v in np.percentile(x, [0, 10, 50, 90, 100]))
         print(f"amend CTAs {int(live.sum())}  items total {int(items.sum())}  tokens total {int(toks.sum())}")
+        tin = (a[:, 6] - base) / 1e3
+        print(f"  entry  us p0/10/50/90/100: {q(tin)}")
+        bnd = a[:, 7] > 0
+        if bnd.any():
+            tb = (a[bnd, 7] - base) / 1e3
+            print(f"  band CTAs {int(bnd.sum())}: band end us p0/10/50/90/100: {q(tb)}  band dur us: {q(tb - tin[bnd])}")
         print(f"  start  us p0/10/50/90/100: {q(t0)}")
         print(f"  end    us p0/10/50/90/100: {q(t1)}")
         has = items > 0
