@@ -60,9 +60,9 @@
 extern "C" {
 #endif
 
-#define MACATTN_ABI_VERSION 13
+#define MACATTN_ABI_VERSION 14
 /* dims of the planar query-ring copy the two-pass scan streams (ring_qp) */
-#define MAC_PLANAR_DIMS 16
+#define MAC_PLANAR_DIMS 8
 
 /* storage modes: dtype of the K/V cache and the query ring; summaries are
  * f32 in MAC_MODE_F32/BF16 and f64 in MAC_MODE_F64 (engine.py:152-153 allows
@@ -127,7 +127,7 @@ typedef struct MacDecodeParams {
   void* ring_q;               /* [B, Hq, W, d]   pre-RoPE queries, storage dtype */
   void* ring_acc;             /* [B, Hq, W, d_v] prefix summary acc (f32 | f64) */
   void* ring_lse;             /* [B, Hq, W]      prefix summary lse (-inf: empty) */
-  void* ring_qp;              /* optional [B, Hq, W, MAC_PLANAR_DIMS] bf16: dims 0..15 of every
+  void* ring_qp;              /* optional [B, Hq, W, MAC_PLANAR_DIMS] bf16: dims 0..7 of every
                                  ring_q row, contiguous per head (32 B per row), kept in step by
                                  the ring write-back; pass 1 of the two-pass scan of the bf16
                                  d = 128 path streams it (NULL: it reads the strided row prefixes
@@ -172,7 +172,7 @@ typedef struct MacDecodeParams {
                                  kernel counts, the append warps publish) */
   int32_t inputs_host;        /* 1: q_pre / k_pre / v_in are device aliases of pinned host memory
                                  (zero-copy).  On the two-pass bf16 d = 128 path the step reads
-                                 them over the host link once: the scan its 16 query dims, the
+                                 them over the host link once: the scan its MAC_PLANAR_DIMS query dims, the
                                  append warps the rest, staging q in the workspace for the later
                                  kernels — no separate input copy before the step */
 } MacDecodeParams;

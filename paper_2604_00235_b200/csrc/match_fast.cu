@@ -156,8 +156,8 @@ __device__ __forceinline__ float dist8_f2(const unsigned long long* q2, uint4 c)
 // ring bytes; when nearly every row survives (a fresh query, all distances
 // ~2d) pass 2 reads the second halves of all rows — the one-pass bytes.  The
 // distance is the one-pass kernel's fp32 sum of squares split in two sums.
-// PLANAR (kQDims = MAC_PLANAR_DIMS = 16): the rows are read from ring_qp, 32 contiguous bytes
-// per row (a contiguous 32 KiB stream per head) instead of strided prefixes of ring_q.
+// PLANAR (kQDims = MAC_PLANAR_DIMS = 8): the rows are read from ring_qp, 16 contiguous bytes
+// per row (a contiguous 16 KiB stream per head at W = 1024) instead of strided prefixes of ring_q.
 template <int kRowsPerCta, int kMinBlocks, int kQDims, bool PLANAR = false, bool HOST = true>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDecodeParams p, int n_match,
                                                                           int do_append, int rotate_only, int plan,
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) front_half_kernel(MacDec
   constexpr int LPR = kQDims / 8;                    // lanes per row (16 B = 8 dims each)
   constexpr int RPW = 32 / LPR;                      // rows per warp-load
   constexpr int kLoads = kRowsPerCta / (8 * RPW);    // loads per lane
-  static_assert(kLoads >= LPR && kLoads % LPR == 0 && (LPR == 8 || LPR == 4 || LPR == 2), "reduce-scatter layout");
+  static_assert(kLoads >= LPR && kLoads % LPR == 0 && (LPR == 8 || LPR == 4 || LPR == 2 || LPR == 1), "reduce-scatter layout");
   constexpr int NF = kLoads / LPR;                   // rows each lane ends up holding
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_append = do_append ? (p.batch * p.n_kv_heads + kThreads / 32 - 1) / (kThreads / 32) : 0;
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(256) verify_kernel(MacDecodeParams p, int rows
 // match_mode 2, after the verify: the full distances of every ring row of the heads the verify
 // deferred (a query with no near-repeat makes every row survive pass 1), one warp per 128-row
 // chunk over the whole GPU instead of one warp walking 1024 rows — the same survivor test and the
-// same fp32 sums as the verify's walk (P(row) + the remaining 112 dims, reduced over 16 lanes), so
+// same fp32 sums as the verify's walk (P(row) + the remaining 128 - MAC_PLANAR_DIMS dims, reduced over 16 lanes), so
 // the argmin is the one the verify would have found.  Chunks publish their best key with an
 // atomic max; the chunk completing a head decides it (finish_decide -> decide_head) and the last
 // head of a group plans the group.
@@ -648,6 +648,7 @@ cudaError_t launch_dense(const MacDecodeParams& p, cudaStream_t st, int qdims) {
   cfg.numAttrs = 1;
   const int nb = band_split(p);
   const int nt = nb > 0 ? piece_target(p) : 0;
+  if (qdims == 8) return cudaLaunchKernelEx(&cfg, dense_kernel<8>, p, nb, nt);
   if (qdims == 16) return cudaLaunchKernelEx(&cfg, dense_kernel<16>, p, nb, nt);
   if (qdims == 32) return cudaLaunchKernelEx(&cfg, dense_kernel<32>, p, nb, nt);
   return cudaLaunchKernelEx(&cfg, dense_kernel<64>, p, nb, nt);
@@ -678,6 +679,9 @@ cudaError_t launch_verify(const MacDecodeParams& p, cudaStream_t st, bool per_he
   const int nb = band_split(p);  // the amend computes the band before its wait (amend_mma.cu)
   const int nt = nb > 0 ? piece_target(p) : 0;
   const int defer = dense_deferred(p) ? 1 : 0;
+  if (qdims == 8)
+    return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 8>, p, rows, nb, nt, defer, n_append, clustered)
+                    : cudaLaunchKernelEx(&cfg, verify_kernel<false, 8>, p, rows, nb, nt, defer, n_append, clustered);
   if (qdims == 16)
     return per_head ? cudaLaunchKernelEx(&cfg, verify_kernel<true, 16>, p, rows, nb, nt, defer, n_append, clustered)
                     : cudaLaunchKernelEx(&cfg, verify_kernel<false, 16>, p, rows, nb, nt, defer, n_append, clustered);
@@ -696,7 +700,7 @@ bool front_fast_supported(const MacDecodeParams& p) {
 }
 
 // Front variants: two-pass match (ring rows per CTA, min CTAs per SM, first-pass dims) =
-// (512, 4, 16) reading ring_qp when given (the product), and the one-pass stream (128, 5).
+// (512, 4, 8) reading ring_qp when given (the product; 16 dims: C3 +1.8 us, r02 session 3), and the one-pass stream (128, 5).
 // Development builds (-DMAC_DEV_KNOBS) add the measured alternatives, selected with
 // MAC_FRONT_VARIANT: 2-3 one-pass (64, 8), (256, 3); 4-7 two-pass (256, 4, 64), (256, 4, 32),
 // (512, 4, 32), (1024, 4, 16).  C3 step (us): 59.8 (0), 67.8 (4); the (256,6) and (512,3)
@@ -715,8 +719,8 @@ struct FrontVariant {
   FrontFn fn_dev, fn_planar_dev;  // the same without the host-input staging (inputs_host == 0)
 };
 static const FrontVariant kFrontVariants[] = {
-    {front_half_kernel<512, 4, 16>, 512, true, 16, front_half_kernel<512, 4, 16, true>,
-     front_half_kernel<512, 4, 16, false, false>, front_half_kernel<512, 4, 16, true, false>},
+    {front_half_kernel<512, 4, 8>, 512, true, 8, front_half_kernel<512, 4, 8, true>,
+     front_half_kernel<512, 4, 8, false, false>, front_half_kernel<512, 4, 8, true, false>},
     {front_bf16_d128_kernel<128, 5>, 128, false, 0, nullptr, front_bf16_d128_kernel<128, 5, false>, nullptr},
 #ifdef MAC_DEV_KNOBS
     {front_bf16_d128_kernel<64, 8>, 64, false, 0, nullptr},

@@ -892,7 +892,7 @@ class StepGraph:
         osz = self.out_host.element_size()
         if self.direct and self.host_inputs and eng._step_mode in (0, 2):
             # the two-pass step reads its inputs from the pinned buffer itself (inputs_host): the
-            # scan its 16 query dims, the append warps the rest, staged for the later kernels; the
+            # scan its MAC_PLANAR_DIMS query dims, the append warps the rest, staged for the later kernels; the
             # complete kernel writes the bf16 output into the pinned output buffer — no I/O launch
             for i, lay in enumerate(self.layers):
                 q, k, v = self._qkv_dev[i]
