@@ -703,7 +703,7 @@ bool front_fast_supported(const MacDecodeParams& p) {
 // (512, 4, 8) reading ring_qp when given (the product; 16 dims: C3 +1.8 us, r02 session 3), and the one-pass stream (128, 5).
 // Development builds (-DMAC_DEV_KNOBS) add the measured alternatives, selected with
 // MAC_FRONT_VARIANT: 2-3 one-pass (64, 8), (256, 3); 4-7 two-pass (256, 4, 64), (256, 4, 32),
-// (512, 4, 32), (1024, 4, 16).  C3 step (us): 59.8 (0), 67.8 (4); the (256,6) and (512,3)
+// (512, 4, 32), (1024, 4, 8), 8: (512, 4, 16) from ring_q.  C3 step (us): 59.8 (0), 67.8 (4); the (256,6) and (512,3)
 // shapes scanned 3.5 and 0.8 us slower than (0); (1024,4,16) scans 2 us faster but its verify
 // (twice the rows per scan-warp summary) takes 1.3 us longer: step 50.4 vs 49.0, C2 34.6 vs
 // 33.7 (r02, same box).  Round-1 alternatives that lost on C3
@@ -728,7 +728,8 @@ static const FrontVariant kFrontVariants[] = {
     {front_half_kernel<256, 4, 64>, 256, true, 64, nullptr},
     {front_half_kernel<256, 4, 32>, 256, true, 32, nullptr},
     {front_half_kernel<512, 4, 32>, 512, true, 32, nullptr},
-    {front_half_kernel<1024, 4, 16>, 1024, true, 16, front_half_kernel<1024, 4, 16, true>},
+    {front_half_kernel<1024, 4, 8>, 1024, true, 8, front_half_kernel<1024, 4, 8, true>},
+    {front_half_kernel<512, 4, 16>, 512, true, 16, nullptr},  // 16 first-pass dims (strided ring_q reads)
 #endif
 };
 
