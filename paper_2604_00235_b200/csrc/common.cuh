@@ -163,6 +163,23 @@ __device__ __forceinline__ int head_lo(int use, int p, int r) {
   return lo < 1 ? 1 : lo;
 }
 
+// ceil(a / b) for 0 <= a, 1 <= b: exact.  On the device, for a < 2^22, through a float quotient
+// and one remainder correction each way (a handful of instructions instead of the ~25 of an integer
+// division): the plan's chunking runs on one thread per GQA group at the end of the verify, where
+// its chain of divisions sat on every step's critical path.
+__host__ __device__ __forceinline__ int cdiv(int a, int b) {
+#ifdef __CUDA_ARCH__
+  if (a >= (1 << 22)) return (a + b - 1) / b;
+  int q = __float2int_rz(__fdividef((float)a, (float)b));
+  int r = a - q * b;
+  if (r < 0) { q -= 1; r += b; }
+  if (r >= b) { q += 1; r -= b; }
+  return q + (r > 0 ? 1 : 0);
+#else
+  return (a + b - 1) / b;
+#endif
+}
+
 struct Chunking {
   int n;    // number of splits
   int len;  // tokens per split (last may be shorter)
@@ -172,13 +189,13 @@ struct Chunking {
 __host__ __device__ __forceinline__ Chunking chunking(int span, int max_chunks, int min_chunk) {
   Chunking c;
   if (span <= 0) { c.n = 0; c.len = 0; return c; }
-  int n = (span + min_chunk - 1) / min_chunk;
+  int n = cdiv(span, min_chunk);
   if (n > max_chunks) n = max_chunks;
   if (n < 1) n = 1;
-  int len = (span + n - 1) / n;
+  int len = cdiv(span, n);
   len = (len + 15) & ~15;
   c.len = len;
-  c.n = (span + len - 1) / len;
+  c.n = cdiv(span, len);
   return c;
 }
 
@@ -223,8 +240,8 @@ __host__ __device__ __forceinline__ BandItems band_items(int m, int r, int nb) {
   const int span = m - s.t0 + 1;
   int n = (span + 15) / 16;
   if (n > nb) n = nb;
-  s.len = (((span + n - 1) / n) + 15) & ~15;
-  s.n = (span + s.len - 1) / s.len;
+  s.len = (cdiv(span, n) + 15) & ~15;
+  s.n = cdiv(span, s.len);
   return s;
 }
 // the plan's split grid with the split band (nb > 0): the piece [grid_start(lo_g), m-r] in
@@ -252,9 +269,9 @@ __host__ __device__ __forceinline__ Chunking plan_chunking(const MacDecodeParams
   // ntarget: bits 0-15 the item count target, bits 16+ the longest item in 16-token sub-tiles
   // (0: 256 tokens, the one-warp amend; the CTA-cooperative TMA amend streams longer items)
   const int tgt = ntarget & 0xffff, max_len = (ntarget >> 16) > 0 ? (ntarget >> 16) * 16 : 256;
-  int n = (span + p.min_chunk - 1) / p.min_chunk;
+  int n = cdiv(span, p.min_chunk);
   if (tgt > 0 && n > tgt) n = tgt;
-  const int n_len = (span + max_len - 1) / max_len;
+  const int n_len = cdiv(span, max_len);
   if (n < n_len) n = n_len;
   if (n_dense > 0 && tgt > 0) {
     const int span_cap = (p.span_chunks > 0 && p.span_chunks < p.max_chunks) ? p.span_chunks : p.max_chunks;
